@@ -1,0 +1,175 @@
+/* occ.h -- C ABI of the B200-native Optimus-CC compression hot path.
+ *
+ * Optimus-CC (arXiv 2301.09830, PAPER.md) compresses three kinds of 3D-parallel
+ * training traffic with PowerSGD-style rank-r low-rank approximation plus error
+ * feedback (§Background, 676-677 §Impl):
+ *   - the backward inter-stage activation gradient (compressed backpropagation
+ *     with lazy error propagation, §CB),
+ *   - data-parallel weight gradients (selective stage compression, PAPER.md:
+ *     627-665 §SC, error feedback PAPER.md:657),
+ *   - the tied-embedding gradient sync, fused into one allreduce over 2D ranks
+ *     (§FE).
+ * For each matrix M (n x m, row-major) one call performs
+ *     A = M + e                (a1, lazy error / error feedback)
+ *     P = A Q_prev             (a2)
+ *     P_hat = orth(P)          (a4; P^T P reduced over ranks first in DP, a3)
+ *     Q = A^T P_hat            (a5; summed over ranks in DP, a6)
+ *     M' = round(P_hat Q^T)    (a7, M's dtype)
+ *     e = A - M'               (a8)    and Q_prev <- Q  (a9, warm start).
+ *
+ * Conventions (every entry point):
+ *  - Tensors are caller-owned DEVICE memory (torch allocations), row-major
+ *    views {ptr, rows, cols, ld (elements), dtype}.  Nothing on the hot path
+ *    allocates device memory; calls are asynchronous and stream ordered.
+ *  - M and recon are OCC_F32 or OCC_BF16; err, P, Q are OCC_F32 always
+ *    (reading C7 in DESIGN.md).  P is n x r, Q is m x r, both contiguous
+ *    (ld == r).  r must be one of 4, 8, 16, 32, 64 and r <= min(n, m).
+ *  - Alignment: 16-byte aligned pointers and ld*elsize % 16 == 0 (128-bit
+ *    loads), else OCC_ERR_ALIGN.  M must not alias err, P or Q.
+ *  - Argument errors are detected on the host before anything is enqueued;
+ *    the buffers are then untouched.  Launch failures map to OCC_ERR_CUDA /
+ *    OCC_ERR_NCCL.  No C++ exception crosses the ABI.  occ_last_error()
+ *    returns a thread-local detail string for the last non-OK status.
+ *  - Workspace: `ws` of at least occ_workspace_bytes(...) bytes of device
+ *    memory, ZEROED ONCE by the caller when allocated; every call leaves it
+ *    in the zeroed state it needs (its grid-barrier words are self-resetting).
+ *    One workspace must not be used by two concurrently executing calls.
+ *  - The library holds no state besides occ_comm handles.
+ */
+#ifndef OCC_H_
+#define OCC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* libocc is built with -fvisibility=hidden; only these declarations export. */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+  OCC_OK = 0,
+  OCC_ERR_INVALID_ARG = 1,
+  OCC_ERR_SHAPE = 2,
+  OCC_ERR_DTYPE = 3,
+  OCC_ERR_RANK = 4,
+  OCC_ERR_ALIGN = 5,
+  OCC_ERR_ALIAS = 6,
+  OCC_ERR_WORKSPACE = 7,
+  OCC_ERR_CUDA = 8,
+  OCC_ERR_NCCL = 9,
+  OCC_ERR_NONFINITE = 10,
+  OCC_ERR_UNSUPPORTED = 11
+} occ_status;
+
+typedef enum { OCC_F32 = 0, OCC_BF16 = 1 } occ_dtype;
+
+/* Row-major matrix view.  ld is the row stride in ELEMENTS. */
+typedef struct {
+  void* ptr;
+  int64_t rows, cols, ld;
+  occ_dtype dtype;
+} occ_mat;
+
+typedef struct occ_comm_s* occ_comm; /* wraps an ncclComm_t */
+
+/* flags */
+enum {
+  OCC_NO_EF = 1u,          /* do not add err (Non-LEP / naive compression); err, if given, receives M - M' */
+  OCC_EF_GLOBAL = 2u,      /* DP only: e_w = A_w - M' instead of the local A_w - P_hat Q_w^T (reading C2) */
+  OCC_CHECK_FINITE = 4u,   /* reserved: set a device status word on non-finite input (not yet implemented) */
+  OCC_FORCE_MULTI = 64u,   /* debug: one launch per phase instead of the fused persistent kernel */
+  OCC_FORCE_TWO_PASS = 128u /* always run the second CholQR pass */
+};
+
+/* Per-call diagnostics written into the workspace (read with occ_read_stats). */
+typedef struct {
+  int32_t fallback_columns; /* columns replaced by their deterministic fallback vector (reading C3) */
+  int32_t second_pass;      /* 1 if the second CholQR pass ran */
+  double kappa_est;         /* ||L||_F * ||L^-1||_F of the first Cholesky factor (>= cond_2(P)) */
+  int32_t path;             /* 1 = fused persistent kernel, 2 = one launch per phase */
+  int32_t grid;             /* CTAs of the persistent kernel */
+} occ_stats;
+
+const char* occ_status_string(occ_status s);
+const char* occ_last_error(void);
+const char* occ_version(void);
+
+/* Bytes of workspace one call on an n x m matrix at rank r needs.  nmat > 1
+ * sizes a DP bucket of nmat matrices of at most n x m each. */
+size_t occ_workspace_bytes(int64_t n, int64_t m, int r, int nmat, uint32_t flags);
+
+/* Q (rows x r, f32, contiguous) <- N(0,1) from a counter-based generator
+ * keyed by `seed` (same seed => same Q on every rank; reading C5). */
+occ_status occ_init_q(occ_mat Q, uint64_t seed, cudaStream_t stream);
+
+/* One compression step on one GPU (the north-star path; SPEC.md:114-136
+ * lowrank_compress / lazy_step).  PAPER.md:383-389 (LEP), 269-270 (PowerSGD).
+ *   M      n x m, f32 or bf16, read only
+ *   err    n x m f32: in e_old, out e_new = A - M'   (may be NULL ptr with OCC_NO_EF)
+ *   Q      m x r f32: in Q_prev, out Q = A^T P_hat   (warm start for the next call)
+ *   P      n x r f32: out P_hat (orthonormal columns)
+ *   recon  n x m in M's dtype: out M' = round(P_hat Q^T), or NULL ptr to skip
+ *          (err is still computed against the rounded M' the receiver would see). */
+occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat recon,
+                        int r, uint32_t flags, void* ws, size_t ws_bytes, cudaStream_t stream);
+
+/* SPEC.md:123-131 lowrank_decompress: out = round(P Q^T).  P n x r, Q m x r
+ * f32; out n x m f32 or bf16. */
+occ_status occ_decompress(occ_mat P, occ_mat Q, occ_mat out, cudaStream_t stream);
+
+/* Data-parallel step over the group `dp` (§SC, 657 EF;
+ * reading C1 order: allreduce-sum P before orthonormalisation, allreduce-sum
+ * Q after Q_w = A_w^T P_hat; one NCCL call per factor for the whole bucket).
+ * For each i < nmat: G[i] (in: local gradient; out: M' = round(P_hat (scale*sum_w Q_w)^T)),
+ * err[i] (EF state), Q[i] (in: Q_prev identical on all ranks; out: scale*sum_w Q_w),
+ * P[i] (out: P_hat).  All matrices share rank r[i] == r[0]. dp == NULL means a
+ * group of one rank (no communication). */
+occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err, const occ_mat* Q,
+                                 const occ_mat* P, const int* r, float scale, uint32_t flags,
+                                 occ_comm dp, void* ws, size_t ws_bytes, cudaStream_t stream);
+
+/* Pipeline backward link, sender side (stage s+1 -> s): occ_compress without
+ * recon, then a grouped ncclSend of P_hat (n x r) and Q (m x r) to `peer`. */
+occ_status occ_send_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, int peer,
+                            uint32_t flags, occ_comm pp, void* ws, size_t ws_bytes,
+                            cudaStream_t stream);
+
+/* Receiver side: grouped ncclRecv of P_hat and Q from `peer`, then
+ * out = round(P_hat Q^T) (bit-identical to the sender's implied M', C8). */
+occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, uint32_t flags,
+                            occ_comm pp, cudaStream_t stream);
+
+/* Fused embedding synchronisation over the 2D-rank group `emb` (PAPER.md:
+ * 598-618).  r == 0: one dense allreduce-sum of scale*G in place (lossless FE).
+ * r > 0: occ_allreduce_factors on the group (compressed FE, reading C14). */
+occ_status occ_embed_sync(occ_mat G, occ_mat err, occ_mat Q, occ_mat P, int r, float scale,
+                          uint32_t flags, occ_comm emb, void* ws, size_t ws_bytes,
+                          cudaStream_t stream);
+
+/* Communicators (NCCL over NVLink / NVSwitch). */
+occ_status occ_get_unique_id(uint8_t id[128]);
+occ_status occ_comm_init(occ_comm* comm, const uint8_t id[128], int nranks, int rank);
+occ_status occ_comm_split(occ_comm parent, int color, int key, occ_comm* out);
+occ_status occ_comm_rank(occ_comm comm, int* rank, int* nranks);
+occ_status occ_comm_destroy(occ_comm comm);
+
+/* Synchronises `stream`, then reports the first pending CUDA / NCCL error. */
+occ_status occ_check_status(cudaStream_t stream, occ_comm comm);
+
+/* Copies the diagnostics of the last call that used `ws` (synchronises). */
+occ_status occ_read_stats(const void* ws, occ_stats* out, cudaStream_t stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCC_H_ */

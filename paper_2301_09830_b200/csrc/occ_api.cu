@@ -1,0 +1,458 @@
+// occ_api.cu -- the extern "C" boundary (include/occ.h): argument validation,
+// workspace carving, orchestration of the step phases and the NCCL exchanges.
+#include "occ.h"
+#include "occ_kernels.cuh"
+#include "occ_internal.h"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+using namespace occ;
+
+struct occ_comm_s {
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+occ_status fail(occ_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+occ_status fail(occ_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+occ_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(OCC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+constexpr int kGeomSms = 148;              // geometry is device independent (B200 SM count)
+constexpr double kTau = 1e-5;              // reading C3
+constexpr double kKappaTwoPass = 1e4;      // CholQR2 trigger on ||L||_F ||L^-1||_F
+constexpr unsigned long long kFbSeed = 0;  // fallback-vector seed (oracle default)
+
+size_t esize(occ_dtype d) { return d == OCC_BF16 ? 2 : 4; }
+
+bool rank_supported(int r) { return r == 4 || r == 8 || r == 16 || r == 32 || r == 64; }
+
+struct Span { uintptr_t lo, hi; };
+Span span_of(const occ_mat& a) {
+  if (!a.ptr || a.rows <= 0) return {0, 0};
+  uintptr_t lo = reinterpret_cast<uintptr_t>(a.ptr);
+  return {lo, lo + (uintptr_t)((a.rows - 1) * a.ld + a.cols) * esize(a.dtype)};
+}
+bool overlap(const occ_mat& a, const occ_mat& b) {
+  Span x = span_of(a), y = span_of(b);
+  if (x.lo == x.hi || y.lo == y.hi) return false;
+  return x.lo < y.hi && y.lo < x.hi;
+}
+
+occ_status check_view(const occ_mat& a, const char* name, int64_t rows, int64_t cols, bool f32_only,
+                      bool contiguous) {
+  if (!a.ptr) return fail(OCC_ERR_INVALID_ARG, "%s: null pointer", name);
+  if (a.dtype != OCC_F32 && a.dtype != OCC_BF16) return fail(OCC_ERR_DTYPE, "%s: unknown dtype %d", name, (int)a.dtype);
+  if (f32_only && a.dtype != OCC_F32) return fail(OCC_ERR_DTYPE, "%s: must be OCC_F32", name);
+  if (a.rows != rows || a.cols != cols)
+    return fail(OCC_ERR_SHAPE, "%s: shape %lldx%lld, expected %lldx%lld", name, (long long)a.rows,
+                (long long)a.cols, (long long)rows, (long long)cols);
+  if (a.ld < a.cols) return fail(OCC_ERR_SHAPE, "%s: ld %lld < cols %lld", name, (long long)a.ld, (long long)a.cols);
+  if (contiguous && a.ld != a.cols) return fail(OCC_ERR_SHAPE, "%s: must be contiguous (ld == cols)", name);
+  if ((reinterpret_cast<uintptr_t>(a.ptr) & 15) != 0) return fail(OCC_ERR_ALIGN, "%s: pointer not 16-byte aligned", name);
+  if ((a.ld * (int64_t)esize(a.dtype)) % 16 != 0) return fail(OCC_ERR_ALIGN, "%s: ld*elsize not a multiple of 16", name);
+  return OCC_OK;
+}
+
+occ_status check_rank(int r, int64_t n, int64_t m) {
+  if (r < 1 || r > std::min(n, m)) return fail(OCC_ERR_RANK, "rank %d outside [1, min(n,m)=%lld]", r, (long long)std::min(n, m));
+  if (!rank_supported(r)) return fail(OCC_ERR_UNSUPPORTED, "rank %d not built (supported: 4, 8, 16, 32, 64)", r);
+  return OCC_OK;
+}
+
+// Validates one (M, err, Q, P, recon) set for the compression step.
+occ_status check_step(const occ_mat& M, const occ_mat& err, const occ_mat& Q, const occ_mat& P,
+                      const occ_mat* recon, int r, uint32_t flags) {
+  if (!M.ptr) return fail(OCC_ERR_INVALID_ARG, "M: null pointer");
+  if (M.rows < 1 || M.cols < 1) return fail(OCC_ERR_SHAPE, "M: empty matrix %lldx%lld", (long long)M.rows, (long long)M.cols);
+  occ_status s = check_rank(r, M.rows, M.cols);
+  if (s) return s;
+  if ((s = check_view(M, "M", M.rows, M.cols, false, false))) return s;
+  if (M.cols % 8 != 0) return fail(OCC_ERR_SHAPE, "M: cols %lld must be a multiple of 8", (long long)M.cols);
+  const bool need_err = !(flags & OCC_NO_EF);
+  if (need_err || err.ptr) {
+    if ((s = check_view(err, "err", M.rows, M.cols, true, false))) return s;
+  }
+  if ((s = check_view(Q, "Q", M.cols, r, true, true))) return s;
+  if ((s = check_view(P, "P", M.rows, r, true, true))) return s;
+  if (recon && recon->ptr) {
+    if ((s = check_view(*recon, "recon", M.rows, M.cols, false, false))) return s;
+    if (recon->dtype != M.dtype) return fail(OCC_ERR_DTYPE, "recon: dtype must equal M's");
+  }
+  const occ_mat* bufs[] = {&err, &Q, &P};
+  const char* names[] = {"err", "Q", "P"};
+  for (int x = 0; x < 3; x++)
+    if (overlap(M, *bufs[x]))
+      return fail(OCC_ERR_ALIAS, "M aliases %s", names[x]);
+  for (int x = 0; x < 3; x++)
+    for (int y = x + 1; y < 3; y++)
+      if (overlap(*bufs[x], *bufs[y])) return fail(OCC_ERR_ALIAS, "%s aliases %s", names[x], names[y]);
+  if (recon && recon->ptr) {
+    for (int x = 0; x < 3; x++)
+      if (overlap(*recon, *bufs[x])) return fail(OCC_ERR_ALIAS, "recon aliases %s", names[x]);
+    if (overlap(*recon, M) && (recon->ptr != M.ptr || recon->ld != M.ld))
+      return fail(OCC_ERR_ALIAS, "recon partially aliases M");
+  }
+  return OCC_OK;
+}
+
+Params base_params(const occ_mat& M, const occ_mat& err, const occ_mat& Q, const occ_mat& P, uint32_t flags) {
+  Params p;
+  memset(&p, 0, sizeof p);
+  p.M = M.ptr;
+  p.ldm = M.ld;
+  p.m_bf16 = M.dtype == OCC_BF16;
+  p.err_in = (flags & OCC_NO_EF) ? nullptr : static_cast<const float*>(err.ptr);
+  p.lde_in = err.ld;
+  p.err_out = static_cast<float*>(err.ptr);
+  p.lde_out = err.ld;
+  p.r_bf16 = M.dtype == OCC_BF16;
+  p.n = (int)M.rows;
+  p.m = (int)M.cols;
+  p.Qprev = static_cast<const float*>(Q.ptr);
+  p.P = static_cast<float*>(P.ptr);
+  p.Qloc = static_cast<float*>(Q.ptr);
+  p.Qrec = static_cast<const float*>(Q.ptr);
+  p.Qstate_out = nullptr;
+  p.scale = 1.0f;
+  p.fb_seed = kFbSeed;
+  p.tau = kTau;
+  p.kappa_thr = kKappaTwoPass;
+  p.force_two_pass = (flags & OCC_FORCE_TWO_PASS) ? 1 : 0;
+  return p;
+}
+
+bool want_multi(uint32_t flags) {
+  if (flags & OCC_FORCE_MULTI) return true;
+  const char* e = getenv("OCC_FORCE_MULTI");
+  return e && e[0] == '1';
+}
+
+occ_status nccl_fail(ncclResult_t r, const char* what) {
+  return fail(OCC_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* occ_status_string(occ_status s) {
+  switch (s) {
+    case OCC_OK: return "OCC_OK";
+    case OCC_ERR_INVALID_ARG: return "OCC_ERR_INVALID_ARG";
+    case OCC_ERR_SHAPE: return "OCC_ERR_SHAPE";
+    case OCC_ERR_DTYPE: return "OCC_ERR_DTYPE";
+    case OCC_ERR_RANK: return "OCC_ERR_RANK";
+    case OCC_ERR_ALIGN: return "OCC_ERR_ALIGN";
+    case OCC_ERR_ALIAS: return "OCC_ERR_ALIAS";
+    case OCC_ERR_WORKSPACE: return "OCC_ERR_WORKSPACE";
+    case OCC_ERR_CUDA: return "OCC_ERR_CUDA";
+    case OCC_ERR_NCCL: return "OCC_ERR_NCCL";
+    case OCC_ERR_NONFINITE: return "OCC_ERR_NONFINITE";
+    case OCC_ERR_UNSUPPORTED: return "OCC_ERR_UNSUPPORTED";
+  }
+  return "OCC_ERR_UNKNOWN";
+}
+
+const char* occ_last_error(void) { return g_err.c_str(); }
+
+const char* occ_version(void) { return "occ 0.1 (sm_100a)"; }
+
+size_t occ_workspace_bytes(int64_t n, int64_t m, int r, int nmat, uint32_t flags) {
+  (void)flags;
+  if (n < 1 || m < 1 || r < 1 || nmat < 1) return 0;
+  Geometry g = make_geometry(n, m, r, kGeomSms);
+  return make_layout(g, nmat).total;
+}
+
+occ_status occ_init_q(occ_mat Q, uint64_t seed, cudaStream_t stream) {
+  occ_status s = check_view(Q, "Q", Q.rows, Q.cols, true, false);
+  if (s) return s;
+  if (Q.rows < 1 || Q.cols < 1) return fail(OCC_ERR_SHAPE, "Q: empty");
+  cudaError_t e = run_init_q(static_cast<float*>(Q.ptr), Q.rows, (int)Q.cols, Q.ld, seed, stream);
+  return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_init_q launch");
+}
+
+occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat recon, int r, uint32_t flags,
+                        void* ws, size_t ws_bytes, cudaStream_t stream) {
+  occ_status s = check_step(M, err, Q, P, &recon, r, flags);
+  if (s) return s;
+  Geometry g = make_geometry(M.rows, M.cols, r, kGeomSms);
+  WsLayout L = make_layout(g, 1);
+  if (!ws || ws_bytes < L.total)
+    return fail(OCC_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, L.total);
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(OCC_ERR_ALIGN, "workspace not 256-byte aligned");
+  Params p = base_params(M, err, Q, P, flags);
+  p.recon = recon.ptr;
+  p.ldr = recon.ptr ? recon.ld : 0;
+  fill_ws(p, g, L, ws);
+  cudaError_t e = run_phases(p, g, 0, 9, want_multi(flags), false, stream);
+  return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_compress launch");
+}
+
+occ_status occ_decompress(occ_mat P, occ_mat Q, occ_mat out, cudaStream_t stream) {
+  if (!out.ptr) return fail(OCC_ERR_INVALID_ARG, "out: null pointer");
+  const int r = (int)P.cols;
+  occ_status s = check_rank(r, out.rows, out.cols);
+  if (s) return s;
+  if ((s = check_view(out, "out", out.rows, out.cols, false, false))) return s;
+  if (out.cols % 8 != 0) return fail(OCC_ERR_SHAPE, "out: cols must be a multiple of 8");
+  if ((s = check_view(P, "P", out.rows, r, true, true))) return s;
+  if ((s = check_view(Q, "Q", out.cols, r, true, true))) return s;
+  if (overlap(out, P) || overlap(out, Q)) return fail(OCC_ERR_ALIAS, "out aliases a factor");
+  Params p;
+  memset(&p, 0, sizeof p);
+  p.n = (int)out.rows;
+  p.m = (int)out.cols;
+  p.P = static_cast<float*>(P.ptr);
+  p.Qrec = static_cast<const float*>(Q.ptr);
+  p.scale = 1.0f;
+  p.recon = out.ptr;
+  p.ldr = out.ld;
+  p.r_bf16 = out.dtype == OCC_BF16;
+  cudaError_t e = run_decompress(p, r, stream);
+  return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_decompress launch");
+}
+
+occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err, const occ_mat* Q, const occ_mat* P,
+                                 const int* r, float scale, uint32_t flags, occ_comm dp, void* ws, size_t ws_bytes,
+                                 cudaStream_t stream) {
+  if (nmat < 1 || !G || !Q || !P || !r) return fail(OCC_ERR_INVALID_ARG, "null array or nmat < 1");
+  if (!(flags & OCC_NO_EF) && !err) return fail(OCC_ERR_INVALID_ARG, "err array required unless OCC_NO_EF");
+  const int R = r[0];
+  int64_t nmax = 0, mmax = 0;
+  for (int i = 0; i < nmat; i++) {
+    if (r[i] != R) return fail(OCC_ERR_RANK, "all matrices of a bucket must share one rank");
+    occ_mat e = err ? err[i] : occ_mat{nullptr, 0, 0, 0, OCC_F32};
+    occ_status s = check_step(G[i], e, Q[i], P[i], nullptr, R, flags);
+    if (s) return fail(s, "matrix %d: %s", i, g_err.c_str());
+    nmax = std::max<int64_t>(nmax, G[i].rows);
+    mmax = std::max<int64_t>(mmax, G[i].cols);
+  }
+  Geometry gmax = make_geometry(nmax, mmax, R, kGeomSms);
+  WsLayout L = make_layout(gmax, nmat);
+  if (!ws || ws_bytes < L.total)
+    return fail(OCC_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, L.total);
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(OCC_ERR_ALIGN, "workspace not 256-byte aligned");
+  const bool multi = want_multi(flags);
+  const bool dpl = !(flags & OCC_EF_GLOBAL);
+  const bool comm = dp && dp->nranks > 1;
+  char* base = static_cast<char*>(ws);
+  float* pb = reinterpret_cast<float*>(base + L.p_bucket);
+  float* qwb = reinterpret_cast<float*>(base + L.qw_bucket);
+  float* qsb = reinterpret_cast<float*>(base + L.qs_bucket);
+  size_t poff[64], qoff[64];
+  if (nmat > 64) return fail(OCC_ERR_INVALID_ARG, "at most 64 matrices per bucket");
+  size_t ptot = 0, qtot = 0;
+  for (int i = 0; i < nmat; i++) {
+    poff[i] = ptot; ptot += (size_t)G[i].rows * R;
+    qoff[i] = qtot; qtot += (size_t)G[i].cols * R;
+  }
+  auto params_for = [&](int i) {
+    occ_mat e = err ? err[i] : occ_mat{nullptr, 0, 0, 0, OCC_F32};
+    Params p = base_params(G[i], e, Q[i], P[i], flags);
+    Geometry g = make_geometry(G[i].rows, G[i].cols, R, kGeomSms);
+    fill_ws(p, g, L, ws);
+    return std::make_pair(p, g);
+  };
+  // (a1-a2) sweep 1 + P reduce for every matrix into the P bucket
+  for (int i = 0; i < nmat; i++) {
+    auto [p, g] = params_for(i);
+    p.P = pb + poff[i];
+    cudaError_t e = run_phases(p, g, 0, 2, multi, dpl, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dp sweep1 launch");
+  }
+  // (a3) allreduce-sum P over the DP group (reading C1)
+  if (comm) {
+    ncclResult_t nr = ncclAllReduce(pb, pb, ptot, ncclFloat, ncclSum, dp->comm, stream);
+    if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(P)");
+  }
+  // (a4-a5) Gram + orthonormalise + sweep 2 + Q reduce into the Q_w bucket
+  for (int i = 0; i < nmat; i++) {
+    auto [p, g] = params_for(i);
+    cudaError_t e = cudaMemcpyAsync(P[i].ptr, pb + poff[i], (size_t)G[i].rows * R * 4, cudaMemcpyDeviceToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "P copy");
+    p.Qloc = qwb + qoff[i];
+    e = run_phases(p, g, 2, 8, multi, dpl, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dp sweep2 launch");
+  }
+  // (a6) allreduce-sum Q
+  float* qsum = qwb;
+  if (comm) {
+    ncclResult_t nr = ncclAllReduce(qwb, qsb, qtot, ncclFloat, ncclSum, dp->comm, stream);
+    if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(Q)");
+    qsum = qsb;
+  }
+  // (a7-a9) M' = round(P_hat (scale sum Q)^T) over G, residual, warm start
+  for (int i = 0; i < nmat; i++) {
+    auto [p, g] = params_for(i);
+    p.Qloc = qwb + qoff[i];
+    p.Qrec = qsum + qoff[i];
+    p.scale = scale;
+    p.Qstate_out = static_cast<float*>(Q[i].ptr);
+    p.dp_local_err = dpl ? 1 : 0;
+    p.recon = G[i].ptr;
+    p.ldr = G[i].ld;
+    cudaError_t e = run_phases(p, g, 8, 9, multi, dpl, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dp reconstruct launch");
+  }
+  return OCC_OK;
+}
+
+occ_status occ_send_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, int peer, uint32_t flags,
+                            occ_comm pp, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (!pp) return fail(OCC_ERR_INVALID_ARG, "pp communicator is null");
+  if (peer < 0 || peer >= pp->nranks || peer == pp->rank) return fail(OCC_ERR_INVALID_ARG, "bad peer %d", peer);
+  occ_mat none = {nullptr, 0, 0, 0, M.dtype};
+  occ_status s = occ_compress(M, err, Q, P, none, r, flags, ws, ws_bytes, stream);
+  if (s) return s;
+  ncclResult_t nr;
+  if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
+  ncclSend(P.ptr, (size_t)M.rows * r, ncclFloat, peer, pp->comm, stream);
+  ncclSend(Q.ptr, (size_t)M.cols * r, ncclFloat, peer, pp->comm, stream);
+  if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclSend(P,Q)");
+  return OCC_OK;
+}
+
+occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, uint32_t flags, occ_comm pp,
+                            cudaStream_t stream) {
+  (void)flags;
+  if (!pp) return fail(OCC_ERR_INVALID_ARG, "pp communicator is null");
+  if (peer < 0 || peer >= pp->nranks || peer == pp->rank) return fail(OCC_ERR_INVALID_ARG, "bad peer %d", peer);
+  if ((int)P.cols != r) return fail(OCC_ERR_SHAPE, "P: cols must equal r");
+  occ_status s = check_view(P, "P", out.rows, r, true, true);
+  if (s) return s;
+  if ((s = check_view(Q, "Q", out.cols, r, true, true))) return s;
+  ncclResult_t nr;
+  if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
+  ncclRecv(P.ptr, (size_t)out.rows * r, ncclFloat, peer, pp->comm, stream);
+  ncclRecv(Q.ptr, (size_t)out.cols * r, ncclFloat, peer, pp->comm, stream);
+  if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclRecv(P,Q)");
+  return occ_decompress(P, Q, out, stream);
+}
+
+occ_status occ_embed_sync(occ_mat G, occ_mat err, occ_mat Q, occ_mat P, int r, float scale, uint32_t flags,
+                          occ_comm emb, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (r > 0) return occ_allreduce_factors(1, &G, &err, &Q, &P, &r, scale, flags, emb, ws, ws_bytes, stream);
+  occ_status s = check_view(G, "G", G.rows, G.cols, false, true);
+  if (s) return s;
+  if (!emb || emb->nranks == 1) {
+    if (scale == 1.0f) return OCC_OK;
+  }
+  ncclDataType_t dt = G.dtype == OCC_BF16 ? ncclBfloat16 : ncclFloat;
+  const size_t count = (size_t)G.rows * G.cols;
+  if (!emb) return fail(OCC_ERR_INVALID_ARG, "emb communicator is null");
+  ncclRedOp_t op;
+  ncclResult_t nr;
+  if (G.dtype == OCC_BF16) {
+    // scalar type must match the data type
+    __nv_bfloat16 sb = __float2bfloat16_rn(scale);
+    nr = ncclRedOpCreatePreMulSum(&op, &sb, dt, ncclScalarHostImmediate, emb->comm);
+  } else {
+    nr = ncclRedOpCreatePreMulSum(&op, &scale, dt, ncclScalarHostImmediate, emb->comm);
+  }
+  if (nr != ncclSuccess) return nccl_fail(nr, "ncclRedOpCreatePreMulSum");
+  nr = ncclAllReduce(G.ptr, G.ptr, count, dt, op, emb->comm, stream);
+  ncclRedOpDestroy(op, emb->comm);
+  if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(EMB)");
+  return OCC_OK;
+}
+
+occ_status occ_get_unique_id(uint8_t id[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  ncclResult_t nr = ncclGetUniqueId(&u);
+  if (nr != ncclSuccess) return nccl_fail(nr, "ncclGetUniqueId");
+  memcpy(id, &u, 128);
+  return OCC_OK;
+}
+
+occ_status occ_comm_init(occ_comm* comm, const uint8_t id[128], int nranks, int rank) {
+  if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(OCC_ERR_INVALID_ARG, "bad comm_init args");
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  occ_comm c = new occ_comm_s;
+  ncclResult_t nr = ncclCommInitRank(&c->comm, nranks, u, rank);
+  if (nr != ncclSuccess) { delete c; return nccl_fail(nr, "ncclCommInitRank"); }
+  c->rank = rank;
+  c->nranks = nranks;
+  *comm = c;
+  return OCC_OK;
+}
+
+occ_status occ_comm_split(occ_comm parent, int color, int key, occ_comm* out) {
+  if (!parent || !out) return fail(OCC_ERR_INVALID_ARG, "bad comm_split args");
+  occ_comm c = new occ_comm_s;
+  ncclResult_t nr = ncclCommSplit(parent->comm, color, key, &c->comm, nullptr);
+  if (nr != ncclSuccess) { delete c; return nccl_fail(nr, "ncclCommSplit"); }
+  if (!c->comm) { delete c; *out = nullptr; return OCC_OK; }  // color == NCCL_SPLIT_NOCOLOR
+  ncclCommUserRank(c->comm, &c->rank);
+  ncclCommCount(c->comm, &c->nranks);
+  *out = c;
+  return OCC_OK;
+}
+
+occ_status occ_comm_rank(occ_comm comm, int* rank, int* nranks) {
+  if (!comm) return fail(OCC_ERR_INVALID_ARG, "null comm");
+  if (rank) *rank = comm->rank;
+  if (nranks) *nranks = comm->nranks;
+  return OCC_OK;
+}
+
+occ_status occ_comm_destroy(occ_comm comm) {
+  if (!comm) return OCC_OK;
+  ncclResult_t nr = ncclCommDestroy(comm->comm);
+  delete comm;
+  return nr == ncclSuccess ? OCC_OK : nccl_fail(nr, "ncclCommDestroy");
+}
+
+occ_status occ_check_status(cudaStream_t stream, occ_comm comm) {
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stream");
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "last error");
+  if (comm) {
+    ncclResult_t ar;
+    ncclResult_t nr = ncclCommGetAsyncError(comm->comm, &ar);
+    if (nr != ncclSuccess) return nccl_fail(nr, "ncclCommGetAsyncError");
+    if (ar != ncclSuccess) return nccl_fail(ar, "nccl async");
+  }
+  return OCC_OK;
+}
+
+occ_status occ_read_stats(const void* ws, occ_stats* out, cudaStream_t stream) {
+  if (!ws || !out) return fail(OCC_ERR_INVALID_ARG, "null ws/out");
+  DevStats d;
+  cudaError_t e = cudaMemcpyAsync(&d, static_cast<const char*>(ws) + 64, sizeof d, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "occ_read_stats");
+  out->fallback_columns = d.fallback_columns;
+  out->second_pass = d.second_pass;
+  out->kappa_est = d.kappa_est;
+  out->path = d.path;
+  out->grid = d.grid;
+  return OCC_OK;
+}
+
+}  // extern "C"

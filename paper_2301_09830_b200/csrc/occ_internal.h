@@ -1,0 +1,33 @@
+// occ_internal.h -- declarations shared by the C-ABI layer and the launch glue.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace occ {
+
+struct Params;
+
+struct Geometry {
+  int64_t n = 0, m = 0;
+  int r = 0;
+  int cs1 = 0, s1 = 0;   // sweep-1 column split width / count
+  int rs2 = 0, s2 = 0;   // sweep-2 row split height / count
+  int ngp = 0;           // Gram partial count (units of 128 rows)
+};
+
+struct WsLayout {
+  size_t bar = 0, p_part = 0, q_part = 0, g_part = 0, g2_part = 0, xy_part = 0;
+  size_t p_bucket = 0, qw_bucket = 0, qs_bucket = 0, total = 0;
+};
+
+Geometry make_geometry(int64_t n, int64_t m, int r, int sms);
+WsLayout make_layout(const Geometry& g, int nmat);
+void fill_ws(Params& p, const Geometry& g, const WsLayout& L, void* ws);
+
+cudaError_t run_phases(const Params& p, const Geometry& g, int ph0, int ph1, bool multi, bool dpl,
+                       cudaStream_t st);
+cudaError_t run_decompress(const Params& p, int r, cudaStream_t st);
+cudaError_t run_init_q(float* q, int64_t rows, int r, int64_t ld, uint64_t seed, cudaStream_t st);
+
+}  // namespace occ

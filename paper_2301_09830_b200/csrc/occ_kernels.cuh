@@ -1,0 +1,738 @@
+// occ_kernels.cuh -- sm_100a device code of the Optimus-CC compression hot path.
+//
+// One compression step (PAPER.md:269-270 PowerSGD power iteration; PAPER.md:
+// 383-389 lazy error propagation; north_star order) is split into phases that
+// each stream over the n x m matrix or its n x r / m x r factors:
+//
+//   A  sweep 1      P_part[s] = (M + e)[:, cols(s)] . Q_prev[cols(s)]      (a1,a2)
+//   B1 P reduce     P = sum_s P_part[s]                                     (a2)
+//   B2 Gram         G_part[u] = P[rows(u)]^T P[rows(u)]   (fp64)            (a4)
+//   C  orth         G = sum_u G_part[u]; Cholesky (fp64) with fallback     (a4)
+//                   columns; P_hat = P L^-T (optionally twice: CholQR2)
+//   D  sweep 2      Q_part[s] = (M + e)[rows(s), :]^T . P_hat[rows(s)]     (a1,a5)
+//   E  Q reduce     Q = sum_s Q_part[s]                                     (a5,a9)
+//   F  reconstruct  M' = round(P_hat Q^T); e_new = (M + e) - M'             (a7,a8)
+//
+// Every phase loops `for (unit = blockIdx.x; unit < units; unit += gridDim.x)`,
+// so the same code runs either as ONE persistent cooperative kernel with a
+// grid barrier between phases (the default path) or as one launch per phase.
+// All cross-CTA reductions are fixed-order (no float atomics): results are
+// bitwise deterministic.  Data produced by other CTAs in the same launch is
+// read with ld.global.cg (L2, never a stale L1 line).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace occ {
+
+constexpr int NT = 256;       // threads per CTA (8 warps)
+constexpr int NW = NT / 32;
+constexpr int B_ROWS = 128;   // rows per unit of phases B1/B2/C
+constexpr int F_ROWS = 64;    // rows per unit of phase F
+
+enum Phase { PH_A = 0, PH_B1 = 1, PH_B2 = 2, PH_C = 3, PH_D = 4, PH_E = 5, PH_F = 6, PH_END = 7 };
+
+struct DevStats {
+  int fallback_columns;
+  int second_pass;
+  double kappa_est;
+  int path;
+  int grid;
+};
+
+struct Params {
+  const void* M; long long ldm; int m_bf16;
+  const float* err_in; long long lde_in;   // nullptr => e_old = 0 (OCC_NO_EF)
+  float* err_out; long long lde_out;       // nullptr => residual not written
+  void* recon; long long ldr; int r_bf16;  // nullptr => M' not written
+  int n, m;
+  const float* Qprev;    // m x R, read in A
+  float* P;              // n x R: raw P after B1, P_hat after C
+  float* Qloc;           // m x R: written by E (local Q_w)
+  const float* Qrec;     // m x R: Q used for M' in F (1 GPU: == Qloc; DP: allreduced sum)
+  float* Qstate_out;     // m x R: if set, F writes scale * Qrec (DP warm start)
+  float scale;
+  int dp_local_err;      // F: e = A - P_hat Qloc^T (DP local convention, reading C2)
+  // workspace
+  float* P_part; int s1; int cs1;
+  float* Q_part; int s2; int rs2;
+  double* G_part;        // [ngp][R(R+1)/2]
+  double* G2_part;       // second-pass Gram partials
+  double* XY_part;       // [ngp][2*R*R]
+  int ngp;
+  unsigned* bar;         // [0] arrivals, [1] exits
+  int* ctl;              // [0] phase-C plan for the per-phase path
+  DevStats* stats;
+  unsigned long long fb_seed;
+  double tau;
+  double kappa_thr;
+  int force_two_pass;
+  int path;
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4 raw, float* a) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    float2 f = __bfloat1622float2(h[q]);
+    a[2 * q] = f.x;
+    a[2 * q + 1] = f.y;
+  }
+}
+
+// A[i][c .. c+W) = M + e for W in {1,2,4,8}; c % W == 0.
+template <int W>
+__device__ __forceinline__ void load_A(const Params& p, int i, int c, float* a) {
+  if (p.m_bf16) {
+    const __nv_bfloat16* row = reinterpret_cast<const __nv_bfloat16*>(p.M) + (size_t)i * p.ldm + c;
+    if constexpr (W == 8) {
+      uint4 raw = __ldcg(reinterpret_cast<const uint4*>(row));
+      bf16x8_to_f32(raw, a);
+    } else if constexpr (W == 4) {
+      uint2 raw = __ldcg(reinterpret_cast<const uint2*>(row));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]);
+      a[0] = f0.x; a[1] = f0.y; a[2] = f1.x; a[3] = f1.y;
+    } else if constexpr (W == 2) {
+      unsigned raw = __ldcg(reinterpret_cast<const unsigned*>(row));
+      float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw));
+      a[0] = f.x; a[1] = f.y;
+    } else {
+      unsigned short raw = __ldcg(reinterpret_cast<const unsigned short*>(row));
+      a[0] = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(&raw));
+    }
+  } else {
+    const float* row = reinterpret_cast<const float*>(p.M) + (size_t)i * p.ldm + c;
+    if constexpr (W >= 4) {
+#pragma unroll
+      for (int q = 0; q < W / 4; q++) {
+        float4 v = __ldcg(reinterpret_cast<const float4*>(row) + q);
+        a[4 * q] = v.x; a[4 * q + 1] = v.y; a[4 * q + 2] = v.z; a[4 * q + 3] = v.w;
+      }
+    } else if constexpr (W == 2) {
+      float2 v = __ldcg(reinterpret_cast<const float2*>(row));
+      a[0] = v.x; a[1] = v.y;
+    } else {
+      a[0] = __ldcg(row);
+    }
+  }
+  if (p.err_in) {
+    const float* er = p.err_in + (size_t)i * p.lde_in + c;
+    if constexpr (W >= 4) {
+#pragma unroll
+      for (int q = 0; q < W / 4; q++) {
+        float4 v = __ldcg(reinterpret_cast<const float4*>(er) + q);
+        a[4 * q] += v.x; a[4 * q + 1] += v.y; a[4 * q + 2] += v.z; a[4 * q + 3] += v.w;
+      }
+    } else if constexpr (W == 2) {
+      float2 v = __ldcg(reinterpret_cast<const float2*>(er));
+      a[0] += v.x; a[1] += v.y;
+    } else {
+      a[0] += __ldcg(er);
+    }
+  }
+}
+
+// splitmix64 fallback vector entry (reading C3; same formula as the oracle,
+// implemented independently): f_j[i] = (splitmix64(seed ^ (j<<32) ^ i) >> 40) * 2^-23 - 1
+__device__ __forceinline__ float fallback_entry(unsigned long long seed, int j, int i) {
+  unsigned long long z = (seed ^ ((unsigned long long)j << 32) ^ (unsigned long long)i) + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z = z ^ (z >> 31);
+  return (float)((double)(z >> 40) * (1.0 / 8388608.0) - 1.0);
+}
+
+__host__ __device__ constexpr int npairs(int R) { return R * (R + 1) / 2; }
+// packed upper-triangle index of (a, b), a <= b
+__device__ __forceinline__ int pidx(int R, int a, int b) { return a * R - (a * (a - 1)) / 2 + (b - a); }
+
+// Fixed-order 8 -> 1 warp tree reduction through shared memory.  Each thread
+// owns V accumulators; slot layout [slot][v][lane] keeps lanes conflict free.
+// On return warp 0 holds the CTA sum.
+template <int V>
+__device__ __forceinline__ void warp_tree_reduce(float (&acc)[V], float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int half = NW / 2; half >= 1; half >>= 1) {
+    __syncthreads();
+    if (warp >= half && warp < 2 * half) {
+      float* s = red + (size_t)(warp - half) * V * 32;
+#pragma unroll
+      for (int v = 0; v < V; v++) s[v * 32 + lane] = acc[v];
+    }
+    __syncthreads();
+    if (warp < half) {
+      const float* s = red + (size_t)warp * V * 32;
+#pragma unroll
+      for (int v = 0; v < V; v++) acc[v] += s[v * 32 + lane];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ configs
+template <int R>
+struct Cfg {
+  static constexpr int A_ROWS = (R <= 32) ? 2 : 1;      // rows per thread in A
+  static constexpr int A_UR = 32 * A_ROWS;              // rows per A unit
+  static constexpr int CPT = (R <= 32) ? 4 : 2;         // columns per thread in D
+  static constexpr int D_CB = 32 * CPT;                 // columns per D unit
+  static constexpr int KS = (R < 16) ? R : 16;          // k-slice of the D reduction
+};
+template <int R, bool DPL>
+struct CfgF {
+  static constexpr int CPT = DPL ? (R <= 16 ? 4 : (R <= 32 ? 2 : 1)) : (R <= 32 ? 4 : 2);
+  static constexpr int CB = 32 * CPT;
+};
+
+// ------------------------------------------------------------------ phase A
+// P_part[s][i][k] = sum_{c in split s} A[i][c] Q_prev[c][k]
+template <int R>
+__device__ void phase_A(const Params& p, float* sm) {
+  constexpr int ROWS = Cfg<R>::A_ROWS, UR = Cfg<R>::A_UR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrb = (p.n + UR - 1) / UR;
+  const int units = nrb * p.s1;
+  float* qs = sm;                          // [cs1][R]
+  float* red = sm + (size_t)p.cs1 * R;     // [4][ROWS*R][32]
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int rb = u % nrb, s = u / nrb;
+    const int c0 = s * p.cs1;
+    const int cw = min(p.cs1, p.m - c0);
+    __syncthreads();
+    const float4* qsrc = reinterpret_cast<const float4*>(p.Qprev + (size_t)c0 * R);
+    for (int x = threadIdx.x; x < cw * R / 4; x += NT) reinterpret_cast<float4*>(qs)[x] = __ldcg(qsrc + x);
+    __syncthreads();
+    float acc[ROWS * R];
+#pragma unroll
+    for (int v = 0; v < ROWS * R; v++) acc[v] = 0.f;
+    for (int cc = warp * 8; cc < cw; cc += NW * 8) {
+      float a[ROWS][8];
+#pragma unroll
+      for (int q = 0; q < ROWS; q++) {
+        const int i = rb * UR + lane + 32 * q;
+        if (i < p.n) load_A<8>(p, i, c0 + cc, a[q]);
+        else {
+#pragma unroll
+          for (int c = 0; c < 8; c++) a[q][c] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const float4* qr = reinterpret_cast<const float4*>(qs + (cc + c) * R);
+#pragma unroll
+        for (int k4 = 0; k4 < R / 4; k4++) {
+          const float4 v = qr[k4];
+#pragma unroll
+          for (int q = 0; q < ROWS; q++) {
+            acc[q * R + 4 * k4 + 0] = fmaf(a[q][c], v.x, acc[q * R + 4 * k4 + 0]);
+            acc[q * R + 4 * k4 + 1] = fmaf(a[q][c], v.y, acc[q * R + 4 * k4 + 1]);
+            acc[q * R + 4 * k4 + 2] = fmaf(a[q][c], v.z, acc[q * R + 4 * k4 + 2]);
+            acc[q * R + 4 * k4 + 3] = fmaf(a[q][c], v.w, acc[q * R + 4 * k4 + 3]);
+          }
+        }
+      }
+    }
+    warp_tree_reduce<ROWS * R>(acc, red);
+    if (warp == 0) {  // stage final sums as [row][k] for a coalesced store
+#pragma unroll
+      for (int q = 0; q < ROWS; q++)
+#pragma unroll
+        for (int k = 0; k < R; k++) red[(lane + 32 * q) * (R + 1) + k] = acc[q * R + k];
+    }
+    __syncthreads();
+    const int r0 = rb * UR;
+    const int nr = min(UR, p.n - r0);
+    float* dst = p.P_part + ((size_t)s * p.n + r0) * R;
+    for (int x = threadIdx.x; x < nr * R; x += NT) dst[x] = red[(x / R) * (R + 1) + (x % R)];
+  }
+}
+
+// ------------------------------------------------------------------ phase B
+// B1: P[i][k] = sum_s P_part[s][i][k];  B2: G_part[u] = P[rows u]^T P[rows u]
+template <int R>
+__device__ void phase_B(const Params& p, float* sm, bool do_reduce, bool do_gram) {
+  const int units = (p.n + B_ROWS - 1) / B_ROWS;
+  float* ps = sm;  // [B_ROWS][R]
+  constexpr int NP = npairs(R);
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
+    __syncthreads();
+    if (do_reduce) {
+      for (int x = threadIdx.x; x < nr * R; x += NT) {
+        float v = 0.f;
+        const float* src = p.P_part + (size_t)r0 * R + x;
+        for (int s = 0; s < p.s1; s++) v += __ldcg(src + (size_t)s * p.n * R);
+        p.P[(size_t)r0 * R + x] = v;
+        ps[x] = v;
+      }
+    } else {
+      for (int x = threadIdx.x; x < nr * R; x += NT) ps[x] = __ldcg(p.P + (size_t)r0 * R + x);
+    }
+    if (!do_gram) continue;
+    __syncthreads();
+    for (int q = threadIdx.x; q < NP; q += NT) {
+      // decode q -> (a, b), a <= b
+      int a = 0, rem = q;
+      while (rem >= R - a) { rem -= R - a; a++; }
+      const int b = a + rem;
+      double g = 0.0;
+      for (int i = 0; i < nr; i++) g = fma((double)ps[i * R + a], (double)ps[i * R + b], g);
+      p.G_part[(size_t)u * NP + q] = g;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ phase C
+// Orthonormalisation by Cholesky-QR with an fp64 Gram (reading C3 / DESIGN.md):
+// column j is degenerate when its squared residual after projection on the
+// previous columns, d_j = G_jj - sum_k L_jk^2, is below tau^2 * G_jj (or
+// G_jj == 0) -- the same test MGS applies to ||v|| < tau * ||p_j||.  A
+// degenerate column is replaced by its fallback vector f_j and the
+// factorisation continues on the modified column set (slow path).
+template <int R>
+struct OrthSmem {
+  double S[R * R];     // Gram, then L (lower)
+  double Li[R * R];    // L^-1 (lower)
+  double X[R * R];     // P^T F (slow path)
+  double Y[R * R];     // F^T F (slow path)
+  double gdiag[R];
+  int rep[R];
+  int flag;
+  double kappa;
+};
+
+template <int R>
+__device__ void reduce_gram(const double* __restrict__ part, int ngp, double* S) {
+  constexpr int NP = npairs(R);
+  for (int q = threadIdx.x; q < NP; q += NT) {
+    int a = 0, rem = q;
+    while (rem >= R - a) { rem -= R - a; a++; }
+    const int b = a + rem;
+    double g = 0.0;
+    for (int u = 0; u < ngp; u++) g += __ldcg(part + (size_t)u * NP + q);
+    S[a * R + b] = g;
+    S[b * R + a] = g;
+  }
+}
+
+// Right-looking Cholesky of S in place (lower triangle).  With detect, stops
+// at the first degenerate column and returns 1.  Uses all threads.
+template <int R>
+__device__ int chol_inplace(double* S, double* gdiag, double tau2, bool detect, int* flag) {
+  for (int x = threadIdx.x; x < R; x += NT) gdiag[x] = S[x * R + x];
+  if (threadIdx.x == 0) *flag = 0;
+  __syncthreads();
+  for (int j = 0; j < R; j++) {
+    if (threadIdx.x == 0) {
+      const double d = S[j * R + j], g = gdiag[j];
+      if (detect && (g == 0.0 || !(d >= tau2 * g))) *flag = 1;
+      else S[j * R + j] = sqrt(d > 0.0 ? d : 1e-300);
+    }
+    __syncthreads();
+    if (*flag) return 1;
+    const double ljj = S[j * R + j];
+    for (int i = j + 1 + threadIdx.x; i < R; i += NT) S[i * R + j] /= ljj;
+    __syncthreads();
+    const int rem = R - 1 - j;
+    for (int x = threadIdx.x; x < rem * rem; x += NT) {
+      const int i = j + 1 + x / rem, k = j + 1 + x % rem;
+      if (k <= i) S[i * R + k] -= S[i * R + j] * S[k * R + j];
+    }
+    __syncthreads();
+  }
+  return 0;
+}
+
+// L^-1 (lower) by forward substitution, one column per thread; returns
+// kappa_est = ||L||_F * ||L^-1||_F (>= cond_2(L) = cond_2(P)).
+template <int R>
+__device__ void tri_inverse(const double* S, double* Li, double* kappa_out) {
+  for (int c = threadIdx.x; c < R; c += NT) {
+    for (int i = 0; i < R; i++) Li[i * R + c] = 0.0;
+    for (int i = c; i < R; i++) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; k++) v -= S[i * R + k] * Li[k * R + c];
+      Li[i * R + c] = v / S[i * R + i];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double nl = 0.0, ni = 0.0;
+    for (int i = 0; i < R; i++)
+      for (int k = 0; k <= i; k++) { nl += S[i * R + k] * S[i * R + k]; ni += Li[i * R + k] * Li[i * R + k]; }
+    *kappa_out = sqrt(nl) * sqrt(ni);
+  }
+  __syncthreads();
+}
+
+// Up-looking Cholesky with column substitution (slow path, thread 0).
+// Gram of the modified column set c_j = rep[j] ? f_j : p_j is read from S (P^T P),
+// X (P^T F) and Y (F^T F).  Result L is written into S's lower triangle.
+template <int R>
+__device__ void chol_substitute(OrthSmem<R>& o, double tau2) {
+  if (threadIdx.x != 0) return;
+  double* L = o.Li;         // scratch for L; S keeps P^T P until the end
+  const double* Gs = o.S;
+  for (int x = 0; x < R * R; x++) L[x] = 0.0;
+  for (int j = 0; j < R; j++) o.rep[j] = 0;
+  auto gram = [&](int a, int b) -> double {  // c_a . c_b
+    const bool ra = o.rep[a], rb = o.rep[b];
+    if (!ra && !rb) return Gs[a * R + b];
+    if (!ra && rb) return o.X[a * R + b];
+    if (ra && !rb) return o.X[b * R + a];
+    return o.Y[a * R + b];
+  };
+  for (int i = 0; i < R; i++) {
+    for (int attempt = 0; attempt < 2; attempt++) {
+      for (int k = 0; k < i; k++) {
+        double v = gram(i, k);
+        for (int l = 0; l < k; l++) v -= L[i * R + l] * L[k * R + l];
+        L[i * R + k] = v / L[k * R + k];
+      }
+      double d = gram(i, i);
+      const double g = d;
+      for (int k = 0; k < i; k++) d -= L[i * R + k] * L[i * R + k];
+      if (attempt == 0 && (g == 0.0 || !(d >= tau2 * g))) { o.rep[i] = 1; continue; }
+      L[i * R + i] = sqrt(d > 0.0 ? d : 1e-300);
+      break;
+    }
+  }
+  for (int x = 0; x < R * R; x++) o.S[x] = L[x];
+}
+
+// P_hat rows [r0, r0+nr) = Pm Li^T in fp64, rounded to fp32, written to dst.
+// Pm[i][b] = rep[b] ? f_b[i] : src[i][b].
+template <int R>
+__device__ void apply_rinv(const float* src, float* dst, int r0, int nr, const double* Li,
+                           const int* rep, bool use_rep, unsigned long long seed, float* ps) {
+  __syncthreads();
+  for (int x = threadIdx.x; x < nr * R; x += NT) {
+    const int i = x / R, b = x % R;
+    ps[x] = (use_rep && rep[b]) ? fallback_entry(seed, b, r0 + i) : __ldcg(src + (size_t)r0 * R + x);
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < nr * R; x += NT) {
+    const int i = x / R, a = x % R;
+    double v = 0.0;
+    for (int b = 0; b <= a; b++) v = fma((double)ps[i * R + b], Li[a * R + b], v);
+    dst[(size_t)r0 * R + x] = (float)v;
+  }
+  __syncthreads();
+}
+
+// Gram partial of rows [r0, r0+nr) of the fp32 matrix `src`, packed, into part[u].
+template <int R>
+__device__ void gram_partial(const float* src, int r0, int nr, double* part_u, float* ps) {
+  constexpr int NP = npairs(R);
+  __syncthreads();
+  for (int x = threadIdx.x; x < nr * R; x += NT) ps[x] = __ldcg(src + (size_t)r0 * R + x);
+  __syncthreads();
+  for (int q = threadIdx.x; q < NP; q += NT) {
+    int a = 0, rem = q;
+    while (rem >= R - a) { rem -= R - a; a++; }
+    const int b = a + rem;
+    double g = 0.0;
+    for (int i = 0; i < nr; i++) g = fma((double)ps[i * R + a], (double)ps[i * R + b], g);
+    part_u[q] = g;
+  }
+}
+
+// C.1: Cholesky-detect.  Returns plan: 0 done, 2 slow path needed (deg), 3 second pass needed.
+template <int R>
+__device__ int phase_C1(const Params& p, OrthSmem<R>& o, float* ps) {
+  const int units = (p.n + B_ROWS - 1) / B_ROWS;
+  const double tau2 = p.tau * p.tau;
+  reduce_gram<R>(p.G_part, p.ngp, o.S);
+  __syncthreads();
+  const int deg = chol_inplace<R>(o.S, o.gdiag, tau2, true, &o.flag);
+  if (deg) {
+    // X = P^T F, Y = F^T F partials for this CTA's rows
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
+      __syncthreads();
+      float* fs = ps + B_ROWS * R;
+      for (int x = threadIdx.x; x < nr * R; x += NT) {
+        ps[x] = __ldcg(p.P + (size_t)r0 * R + x);
+        fs[x] = fallback_entry(p.fb_seed, x % R, r0 + x / R);
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < 2 * R * R; q += NT) {
+        const int which = q / (R * R), a = (q / R) % R, b = q % R;
+        const float* lhs = which ? fs : ps;
+        double g = 0.0;
+        for (int i = 0; i < nr; i++) g = fma((double)lhs[i * R + a], (double)fs[i * R + b], g);
+        p.XY_part[(size_t)u * 2 * R * R + q] = g;
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.ctl[0] = 2;
+    return 2;
+  }
+  tri_inverse<R>(o.S, o.Li, &o.kappa);
+  const bool need2 = p.force_two_pass || o.kappa > p.kappa_thr;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
+    apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, false, p.fb_seed, ps);
+    if (need2) gram_partial<R>(p.P, r0, nr, p.G2_part + (size_t)u * npairs(R), ps);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.ctl[0] = need2 ? 3 : 0;
+    p.stats->fallback_columns = 0;
+    p.stats->second_pass = need2 ? 1 : 0;
+    p.stats->kappa_est = o.kappa;
+  }
+  return need2 ? 3 : 0;
+}
+
+// C.2: slow path with fallback substitution.  Returns 0 or 3.
+template <int R>
+__device__ int phase_C2(const Params& p, OrthSmem<R>& o, float* ps) {
+  const int units = (p.n + B_ROWS - 1) / B_ROWS;
+  const double tau2 = p.tau * p.tau;
+  reduce_gram<R>(p.G_part, p.ngp, o.S);
+  for (int q = threadIdx.x; q < 2 * R * R; q += NT) {
+    double g = 0.0;
+    for (int u = 0; u < p.ngp; u++) g += __ldcg(p.XY_part + (size_t)u * 2 * R * R + q);
+    if (q < R * R) o.X[q] = g; else o.Y[q - R * R] = g;
+  }
+  __syncthreads();
+  chol_substitute<R>(o, tau2);
+  __syncthreads();
+  tri_inverse<R>(o.S, o.Li, &o.kappa);
+  const bool need2 = p.force_two_pass || o.kappa > p.kappa_thr;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
+    apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, true, p.fb_seed, ps);
+    if (need2) gram_partial<R>(p.P, r0, nr, p.G2_part + (size_t)u * npairs(R), ps);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int cnt = 0;
+    for (int j = 0; j < R; j++) cnt += o.rep[j];
+    p.ctl[0] = need2 ? 3 : 0;
+    p.stats->fallback_columns = cnt;
+    p.stats->second_pass = need2 ? 1 : 0;
+    p.stats->kappa_est = o.kappa;
+  }
+  return need2 ? 3 : 0;
+}
+
+// C.3: second CholQR pass on the (fp32-rounded) P_hat of the first pass.
+template <int R>
+__device__ void phase_C3(const Params& p, OrthSmem<R>& o, float* ps) {
+  const int units = (p.n + B_ROWS - 1) / B_ROWS;
+  reduce_gram<R>(p.G2_part, p.ngp, o.S);
+  __syncthreads();
+  chol_inplace<R>(o.S, o.gdiag, 0.0, false, &o.flag);
+  double dummy;
+  tri_inverse<R>(o.S, o.Li, &dummy);
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
+    apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, false, p.fb_seed, ps);
+  }
+}
+
+// ------------------------------------------------------------------ phase D
+// Q_part[s][j][k] = sum_{i in split s} A[i][j] P_hat[i][k]
+template <int R>
+__device__ void phase_D(const Params& p, float* sm) {
+  constexpr int CPT = Cfg<R>::CPT, CB = Cfg<R>::D_CB, KS = Cfg<R>::KS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ncb = (p.m + CB - 1) / CB;
+  const int units = ncb * p.s2;
+  float* phs = sm;                          // [rs2][R]
+  float* red = sm + (size_t)p.rs2 * R;      // [4][CPT*KS][32]
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int cb = u % ncb, s = u / ncb;
+    const int r0 = s * p.rs2, nr = min(p.rs2, p.n - r0);
+    const int c = cb * CB + lane * CPT;
+    const bool cok = c < p.m;
+    __syncthreads();
+    for (int x = threadIdx.x; x < nr * R / 4; x += NT)
+      reinterpret_cast<float4*>(phs)[x] = __ldcg(reinterpret_cast<const float4*>(p.P + (size_t)r0 * R) + x);
+    __syncthreads();
+    float acc[CPT * R];
+#pragma unroll
+    for (int v = 0; v < CPT * R; v++) acc[v] = 0.f;
+    if (cok) {
+      for (int ii = warp; ii < nr; ii += NW) {
+        float a[CPT];
+        load_A<CPT>(p, r0 + ii, c, a);
+        const float4* ph = reinterpret_cast<const float4*>(phs + ii * R);
+#pragma unroll
+        for (int k4 = 0; k4 < R / 4; k4++) {
+          const float4 v = ph[k4];
+#pragma unroll
+          for (int q = 0; q < CPT; q++) {
+            acc[q * R + 4 * k4 + 0] = fmaf(a[q], v.x, acc[q * R + 4 * k4 + 0]);
+            acc[q * R + 4 * k4 + 1] = fmaf(a[q], v.y, acc[q * R + 4 * k4 + 1]);
+            acc[q * R + 4 * k4 + 2] = fmaf(a[q], v.z, acc[q * R + 4 * k4 + 2]);
+            acc[q * R + 4 * k4 + 3] = fmaf(a[q], v.w, acc[q * R + 4 * k4 + 3]);
+          }
+        }
+      }
+    }
+    // reduce over warps in k-slices of KS
+    float* dst = p.Q_part + (size_t)s * p.m * R;
+#pragma unroll
+    for (int k0 = 0; k0 < R; k0 += KS) {
+      float sl[CPT * KS];
+#pragma unroll
+      for (int q = 0; q < CPT; q++)
+#pragma unroll
+        for (int k = 0; k < KS; k++) sl[q * KS + k] = acc[q * R + k0 + k];
+      warp_tree_reduce<CPT * KS>(sl, red);
+      if (warp == 0 && cok) {
+#pragma unroll
+        for (int q = 0; q < CPT; q++) {
+          float* d = dst + (size_t)(c + q) * R + k0;
+#pragma unroll
+          for (int k4 = 0; k4 < KS / 4; k4++)
+            reinterpret_cast<float4*>(d)[k4] =
+                make_float4(sl[q * KS + 4 * k4], sl[q * KS + 4 * k4 + 1], sl[q * KS + 4 * k4 + 2], sl[q * KS + 4 * k4 + 3]);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ phase E
+template <int R>
+__device__ void phase_E(const Params& p) {
+  constexpr int UC = 32;   // columns per unit
+  const int units = (p.m + UC - 1) / UC;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int c0 = u * UC, nc = min(UC, p.m - c0);
+    for (int x = threadIdx.x; x < nc * R; x += NT) {
+      const float* src = p.Q_part + (size_t)c0 * R + x;
+      float v = 0.f;
+      for (int s = 0; s < p.s2; s++) v += __ldcg(src + (size_t)s * p.m * R);
+      p.Qloc[(size_t)c0 * R + x] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ phase F
+// M' = round(P_hat (scale*Qrec)^T);  e_new = A - M'  (or A - P_hat Qloc^T, DP local)
+template <int R, bool DPL>
+__device__ void phase_F(const Params& p, float* sm) {
+  constexpr int CPT = CfgF<R, DPL>::CPT, CB = CfgF<R, DPL>::CB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ncb = (p.m + CB - 1) / CB;
+  const int nrb = (p.n + F_ROWS - 1) / F_ROWS;
+  const int units = ncb * nrb;
+  float* phs = sm;  // [F_ROWS][R]
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int rb = u % nrb, cb = u / nrb;
+    const int r0 = rb * F_ROWS, nr = min(F_ROWS, p.n - r0);
+    const int c = cb * CB + lane * CPT;
+    const bool cok = c < p.m;
+    __syncthreads();
+    for (int x = threadIdx.x; x < nr * R / 4; x += NT)
+      reinterpret_cast<float4*>(phs)[x] = __ldcg(reinterpret_cast<const float4*>(p.P + (size_t)r0 * R) + x);
+    __syncthreads();
+    if (!cok) continue;
+    float qv[CPT * R];
+    float ql[DPL ? CPT * R : 1];
+#pragma unroll
+    for (int q = 0; q < CPT; q++) {
+      const float4* src = reinterpret_cast<const float4*>(p.Qrec + (size_t)(c + q) * R);
+#pragma unroll
+      for (int k4 = 0; k4 < R / 4; k4++) {
+        float4 v = __ldcg(src + k4);
+        qv[q * R + 4 * k4 + 0] = p.scale * v.x; qv[q * R + 4 * k4 + 1] = p.scale * v.y;
+        qv[q * R + 4 * k4 + 2] = p.scale * v.z; qv[q * R + 4 * k4 + 3] = p.scale * v.w;
+      }
+      if constexpr (DPL) {
+        const float4* sl = reinterpret_cast<const float4*>(p.Qloc + (size_t)(c + q) * R);
+#pragma unroll
+        for (int k4 = 0; k4 < R / 4; k4++) {
+          float4 v = __ldcg(sl + k4);
+          ql[q * R + 4 * k4 + 0] = v.x; ql[q * R + 4 * k4 + 1] = v.y;
+          ql[q * R + 4 * k4 + 2] = v.z; ql[q * R + 4 * k4 + 3] = v.w;
+        }
+      }
+    }
+    if (p.Qstate_out && rb == 0) {
+#pragma unroll
+      for (int q = 0; q < CPT; q++)
+#pragma unroll
+        for (int k4 = 0; k4 < R / 4; k4++)
+          reinterpret_cast<float4*>(p.Qstate_out + (size_t)(c + q) * R)[k4] =
+              make_float4(qv[q * R + 4 * k4], qv[q * R + 4 * k4 + 1], qv[q * R + 4 * k4 + 2], qv[q * R + 4 * k4 + 3]);
+    }
+    for (int ii = warp; ii < nr; ii += NW) {
+      const int i = r0 + ii;
+      float a[CPT];
+      const bool need_a = p.err_out != nullptr;
+      if (need_a) load_A<CPT>(p, i, c, a);
+      const float4* ph = reinterpret_cast<const float4*>(phs + ii * R);
+      float mr[CPT], ml[CPT];
+#pragma unroll
+      for (int q = 0; q < CPT; q++) { mr[q] = 0.f; ml[q] = 0.f; }
+#pragma unroll
+      for (int k4 = 0; k4 < R / 4; k4++) {
+        const float4 v = ph[k4];
+#pragma unroll
+        for (int q = 0; q < CPT; q++) {
+          mr[q] = fmaf(v.x, qv[q * R + 4 * k4 + 0], mr[q]);
+          mr[q] = fmaf(v.y, qv[q * R + 4 * k4 + 1], mr[q]);
+          mr[q] = fmaf(v.z, qv[q * R + 4 * k4 + 2], mr[q]);
+          mr[q] = fmaf(v.w, qv[q * R + 4 * k4 + 3], mr[q]);
+          if constexpr (DPL) {
+            ml[q] = fmaf(v.x, ql[q * R + 4 * k4 + 0], ml[q]);
+            ml[q] = fmaf(v.y, ql[q * R + 4 * k4 + 1], ml[q]);
+            ml[q] = fmaf(v.z, ql[q * R + 4 * k4 + 2], ml[q]);
+            ml[q] = fmaf(v.w, ql[q * R + 4 * k4 + 3], ml[q]);
+          }
+        }
+      }
+      // round M' to the output dtype (reading C7): the residual is taken
+      // against exactly what the receiver decodes.
+      if (p.r_bf16) {
+#pragma unroll
+        for (int q = 0; q < CPT; q++) mr[q] = __bfloat162float(__float2bfloat16_rn(mr[q]));
+      }
+      if (p.recon) {
+        if (p.r_bf16) {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.recon) + (size_t)i * p.ldr + c;
+#pragma unroll
+          for (int q = 0; q < CPT; q++) dst[q] = __float2bfloat16_rn(mr[q]);
+        } else {
+          float* dst = reinterpret_cast<float*>(p.recon) + (size_t)i * p.ldr + c;
+          if constexpr (CPT == 4) *reinterpret_cast<float4*>(dst) = make_float4(mr[0], mr[1], mr[2], mr[3]);
+          else if constexpr (CPT == 2) *reinterpret_cast<float2*>(dst) = make_float2(mr[0], mr[1]);
+          else dst[0] = mr[0];
+        }
+      }
+      if (need_a) {
+        float e[CPT];
+#pragma unroll
+        for (int q = 0; q < CPT; q++) e[q] = a[q] - (DPL ? ml[q] : mr[q]);
+        float* dst = p.err_out + (size_t)i * p.lde_out + c;
+        if constexpr (CPT == 4) *reinterpret_cast<float4*>(dst) = make_float4(e[0], e[1], e[2], e[3]);
+        else if constexpr (CPT == 2) *reinterpret_cast<float2*>(dst) = make_float2(e[0], e[1]);
+        else dst[0] = e[0];
+      }
+    }
+  }
+}
+
+}  // namespace occ

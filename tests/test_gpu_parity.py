@@ -1,0 +1,226 @@
+"""GPU parity (-m gpu): the CUDA path through the C-ABI vs the fp64 oracle on
+the same seeded inputs.
+
+Tolerances (north_star): relative Frobenius error of M' and e_new (against
+||A||_F) <= 1e-4 for fp32, <= 1e-2 for bf16 inputs/outputs; factor
+orthonormality ||P_hat^T P_hat - I||_F <= 1e-5.  P_hat and Q are also compared
+column by column where the factor is unique (no fallback fired, kappa(P) small;
+reading C4).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2301_09830_b200 import build as occ_build  # noqa: E402
+from paper_2301_09830_b200 import occ  # noqa: E402
+
+TOL32, TOLBF, TOLORTH = 1e-4, 1e-2, 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    occ_build.build()
+    occ.lib()
+
+
+def to_dev(x, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda").to(dtype)
+
+
+def run_gpu(M, e, Q0, r, *, bf16=False, flags=0, recon=True):
+    n, m = M.shape
+    Md = to_dev(M, torch.bfloat16 if bf16 else torch.float32)
+    Ed = to_dev(e) if e is not None else None
+    Qd = to_dev(Q0)
+    Pd = torch.empty(n, r, device="cuda")
+    Rd = torch.empty_like(Md) if recon else None
+    ws = occ.occ_compress(Md, Ed, Qd, Pd, Rd, r=r, flags=flags)
+    torch.cuda.synchronize()
+    st = occ.occ_read_stats(ws)
+    M_used = Md.double().cpu().numpy()   # bf16-rounded input as the GPU saw it
+    return {"P_hat": Pd.double().cpu().numpy(), "Q": Qd.double().cpu().numpy(),
+            "recon": Rd.double().cpu().numpy() if recon else None,
+            "err": Ed.double().cpu().numpy() if Ed is not None else None, "stats": st, "M_used": M_used}
+
+
+def rel(a, b, ref):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(ref), 1e-300)
+
+
+def check_step(g, o, A, *, tol, check_factors=True):
+    r = g["P_hat"].shape[1]
+    orth = np.linalg.norm(g["P_hat"].T @ g["P_hat"] - np.eye(r))
+    assert orth <= TOLORTH, orth
+    if g["recon"] is not None:
+        assert rel(g["recon"], o["recon"], A) <= tol
+    if g["err"] is not None:
+        assert rel(g["err"], o["err"], A) <= tol
+    if check_factors and not o["fallbacks"]:
+        assert rel(g["P_hat"], o["P_hat"], o["P_hat"]) <= 100 * tol
+        assert rel(g["Q"], o["Q"], o["Q"]) <= tol * 10
+
+
+SHAPES = [
+    (128, 256, 4, "D1"),      # C1 (BASELINE configs[0])
+    (128, 256, 4, "D2"),
+    (200, 136, 8, "D2"),      # ragged tails in every tiling
+    (1000, 392, 16, "D2"),
+    (1024, 3072, 16, "D2"),   # north-star target T
+    (777, 1208, 32, "D2"),
+    (640, 1024, 64, "D2"),
+]
+
+
+@pytest.mark.parametrize("n,m,r,dist", SHAPES)
+def test_compress_matches_oracle_fp32(n, m, r, dist):
+    M = synth.make(dist, n, m, 1000 + n + r)
+    e = synth.e0(n, m, 1001 + n, like=M)
+    Q0 = synth.q0(m, r, 7)
+    g = run_gpu(M, e, Q0, r)
+    o = oracle.compress_step(M, e, Q0)
+    A = M.astype(np.float64) + e
+    check_step(g, o, A, tol=TOL32)
+    assert g["stats"]["fallback_columns"] == len(o["fallbacks"])
+
+
+@pytest.mark.parametrize("n,m,r", [(256, 512, 16), (1024, 3072, 16), (1000, 392, 8)])
+def test_compress_bf16(n, m, r):
+    M = synth.d2_gradlike(n, m, 31)
+    e = synth.e0(n, m, 32, like=M)
+    Q0 = synth.q0(m, r, 33)
+    g = run_gpu(M, e, Q0, r, bf16=True)
+    o = oracle.compress_step(g["M_used"], e, Q0, out_dtype="bf16")
+    A = g["M_used"] + e
+    check_step(g, o, A, tol=TOLBF, check_factors=False)
+    # EF identity on the GPU: M'_bf16 + e_new == A up to fp32 rounding (reading C7)
+    assert rel(g["recon"] + g["err"], A, A) <= 1e-6
+
+
+def test_no_ef_and_null_err():
+    n, m, r = 256, 512, 8
+    M = synth.d2_gradlike(n, m, 41)
+    Q0 = synth.q0(m, r, 42)
+    g = run_gpu(M, None, Q0, r, flags=occ.OCC_NO_EF)
+    o = oracle.compress_step(M, None, Q0, no_ef=True)
+    check_step(g, o, M.astype(np.float64), tol=TOL32)
+
+
+def test_fused_and_per_phase_paths_bitwise_equal_and_deterministic():
+    n, m, r = 1000, 1208, 16
+    M = synth.d2_gradlike(n, m, 51)
+    e = synth.e0(n, m, 52, like=M)
+    Q0 = synth.q0(m, r, 53)
+    a = run_gpu(M, e, Q0, r)
+    b = run_gpu(M, e, Q0, r, flags=occ.OCC_FORCE_MULTI)
+    c = run_gpu(M, e, Q0, r)
+    assert a["stats"]["path"] == 1 and b["stats"]["path"] == 2
+    for k in ("P_hat", "Q", "recon", "err"):
+        assert np.array_equal(a[k], b[k]), k
+        assert np.array_equal(a[k], c[k]), k
+
+
+def test_zero_input_all_fallbacks():
+    n, m, r = 300, 264, 8
+    M = np.zeros((n, m), np.float32)
+    g = run_gpu(M, np.zeros((n, m), np.float32), synth.q0(m, r, 3), r)
+    assert np.all(g["recon"] == 0) and np.all(g["err"] == 0)
+    assert g["stats"]["fallback_columns"] == r
+    o = oracle.compress_step(M, None, synth.q0(m, r, 3))
+    assert np.linalg.norm(g["P_hat"].T @ g["P_hat"] - np.eye(r)) <= TOLORTH
+    # same fallback vectors, same order -> same P_hat (counter-based generator on both sides)
+    np.testing.assert_allclose(g["P_hat"], o["P_hat"], atol=1e-6)
+
+
+@pytest.mark.parametrize("k,r", [(2, 8), (5, 16), (16, 16)])
+def test_exact_low_rank_recovered(k, r):
+    n, m = 512, 640
+    M = synth.d4_exact_lowrank(n, m, k, seed=61)
+    g = run_gpu(M, None, synth.q0(m, r, 62), r, flags=occ.OCC_NO_EF)
+    assert np.linalg.norm(g["recon"] - M) <= 1e-5 * np.linalg.norm(M)
+    assert g["stats"]["fallback_columns"] == r - k
+    assert np.linalg.norm(g["P_hat"].T @ g["P_hat"] - np.eye(r)) <= TOLORTH
+
+
+def test_forced_second_pass():
+    n, m, r = 1024, 1024, 16
+    M = synth.d2_gradlike(n, m, 71)
+    Q0 = synth.q0(m, r, 72)
+    g = run_gpu(M, None, Q0, r, flags=occ.OCC_NO_EF | occ.OCC_FORCE_TWO_PASS)
+    assert g["stats"]["second_pass"] == 1
+    o = oracle.compress_step(M, None, Q0, no_ef=True)
+    check_step(g, o, M.astype(np.float64), tol=TOL32)
+
+
+def test_lep_stream_free_running_16_steps():
+    n, m, r, T = 512, 768, 16, 16
+    Ms = synth.d3_lep_stream(n, m, 81, T)
+    Q0 = synth.q0(m, r, 82)
+    Md = torch.empty(n, m, device="cuda")
+    Ed = torch.zeros(n, m, device="cuda")
+    Qd = to_dev(Q0)
+    Pd = torch.empty(n, r, device="cuda")
+    Rd = torch.empty(n, m, device="cuda")
+    ws = occ.alloc_workspace(n, m, r)
+    e_o = np.zeros((n, m))
+    Q_o = Q0.astype(np.float64)
+    tot_g = np.zeros((n, m))
+    for t, Mt in enumerate(Ms):
+        Md.copy_(to_dev(Mt))
+        occ.occ_compress(Md, Ed, Qd, Pd, Rd, r=r, ws=ws)
+        A = Mt.astype(np.float64) + e_o
+        o = oracle.compress_step(Mt, e_o, Q_o)
+        e_o, Q_o = o["err"], o["Q"]
+        rg = Rd.double().cpu().numpy()
+        tot_g += rg
+        assert rel(rg, o["recon"], A) <= TOL32, t
+    # telescoping on the GPU's own numbers: sum M'_t = sum M_t + e_0 - e_T (P9)
+    expect = sum(x.astype(np.float64) for x in Ms) - Ed.double().cpu().numpy()
+    assert rel(tot_g, expect, expect) <= 1e-5
+
+
+def test_decompress_matches_oracle():
+    n, m, r = 700, 1032, 16
+    rng = np.random.default_rng(91)
+    P = rng.standard_normal((n, r)).astype(np.float32)
+    Q = rng.standard_normal((m, r)).astype(np.float32)
+    for dt, tol in ((torch.float32, 1e-6), (torch.bfloat16, 1e-2)):
+        out = torch.empty(n, m, device="cuda", dtype=dt)
+        occ.occ_decompress(to_dev(P), to_dev(Q), out)
+        torch.cuda.synchronize()
+        o = oracle.decompress(P, Q, out_dtype="f32" if dt == torch.float32 else "bf16")
+        assert rel(out.double().cpu().numpy(), o, o) <= tol
+
+
+def test_dp_single_rank_matches_oracle():
+    # occ_allreduce_factors with no communicator = a DP group of one rank
+    n, m, r = 512, 1024, 16
+    M = synth.d2_gradlike(n, m, 101)
+    e = synth.e0(n, m, 102, like=M)
+    Q0 = synth.q0(m, r, 103)
+    Gd, Ed, Qd = to_dev(M), to_dev(e), to_dev(Q0)
+    Pd = torch.empty(n, r, device="cuda")
+    occ.occ_allreduce_factors([Gd], [Ed], [Qd], [Pd], r, 1.0)
+    torch.cuda.synchronize()
+    o = oracle.dp_step([M], [e], Q0, scale=1.0)
+    A = M.astype(np.float64) + e
+    assert rel(Gd.double().cpu().numpy(), o["recon"], A) <= TOL32
+    assert rel(Ed.double().cpu().numpy(), o["err"][0], A) <= TOL32
+    assert rel(Qd.double().cpu().numpy(), o["Q"], o["Q"]) <= 1e-3
+
+
+def test_init_q_is_standard_normal_and_seeded():
+    Q = torch.empty(4096, 16, device="cuda")
+    occ.occ_init_q(Q, 1234)
+    Q2 = torch.empty_like(Q)
+    occ.occ_init_q(Q2, 1234)
+    torch.cuda.synchronize()
+    assert torch.equal(Q, Q2)
+    x = Q.double().cpu().numpy()
+    assert abs(x.mean()) < 0.02 and abs(x.std() - 1) < 0.02
