@@ -94,6 +94,7 @@ typedef struct {
   double kappa_est;         /* ||L||_F * ||L^-1||_F of the first Cholesky factor (>= cond_2(P)) */
   int32_t path;             /* 1 = fused persistent kernel, 2 = one launch per phase */
   int32_t grid;             /* CTAs of the persistent kernel */
+  uint64_t t_ns[12];        /* fused path: %globaltimer when CTA 0 entered phase k (0 = A, 1 = B, 3 = C, 6 = D, 7 = E, 8 = F, 9 = end) */
 } occ_stats;
 
 const char* occ_status_string(occ_status s);

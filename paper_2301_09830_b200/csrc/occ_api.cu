@@ -149,6 +149,11 @@ bool want_multi(uint32_t flags) {
   return e && e[0] == '1';
 }
 
+bool want_v1() {
+  const char* e = getenv("OCC_PATH");
+  return e && e[0] == 'v' && e[1] == '1';
+}
+
 occ_status nccl_fail(ncclResult_t r, const char* what) {
   return fail(OCC_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
 }
@@ -207,7 +212,13 @@ occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat re
   p.recon = recon.ptr;
   p.ldr = recon.ptr ? recon.ld : 0;
   fill_ws(p, g, L, ws);
-  cudaError_t e = run_phases(p, g, 0, 9, want_multi(flags), false, stream);
+  const bool multi = want_multi(flags);
+  if (!multi && !want_v1() && L.v2_tail_bytes > 0) {
+    cudaError_t e2 = run_v2(p, r, static_cast<char*>(ws) + L.v2_tail, L.v2_tail_bytes, kGeomSms, stream);
+    if (e2 == cudaSuccess) return OCC_OK;
+    if (e2 != cudaErrorNotSupported) return cuda_fail(e2, "occ_compress (fused v2) launch");
+  }
+  cudaError_t e = run_phases(p, g, 0, 9, multi, false, stream);
   return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_compress launch");
 }
 
@@ -452,6 +463,7 @@ occ_status occ_read_stats(const void* ws, occ_stats* out, cudaStream_t stream) {
   out->kappa_est = d.kappa_est;
   out->path = d.path;
   out->grid = d.grid;
+  for (int k = 0; k < 12; k++) out->t_ns[k] = d.t_ns[k];
   return OCC_OK;
 }
 

@@ -18,7 +18,7 @@ struct Geometry {
 
 struct WsLayout {
   size_t bar = 0, p_part = 0, q_part = 0, g_part = 0, g2_part = 0, xy_part = 0;
-  size_t p_bucket = 0, qw_bucket = 0, qs_bucket = 0, total = 0;
+  size_t p_bucket = 0, qw_bucket = 0, qs_bucket = 0, v2_tail = 0, v2_tail_bytes = 0, total = 0;
 };
 
 Geometry make_geometry(int64_t n, int64_t m, int r, int sms);
@@ -28,6 +28,8 @@ void fill_ws(Params& p, const Geometry& g, const WsLayout& L, void* ws);
 cudaError_t run_phases(const Params& p, const Geometry& g, int ph0, int ph1, bool multi, bool dpl,
                        cudaStream_t st);
 cudaError_t run_decompress(const Params& p, int r, cudaStream_t st);
+size_t v2_tail_bytes(int64_t n, int64_t m, int r, int sms);
+cudaError_t run_v2(const Params& p, int r, void* ws_tail, size_t tail_avail, int sms, cudaStream_t st);
 cudaError_t run_init_q(float* q, int64_t rows, int r, int64_t ld, uint64_t seed, cudaStream_t st);
 
 }  // namespace occ

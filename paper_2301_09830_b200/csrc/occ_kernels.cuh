@@ -39,7 +39,14 @@ struct DevStats {
   double kappa_est;
   int path;
   int grid;
+  unsigned long long t_ns[12];   // %globaltimer at phase boundaries (CTA 0)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct Params {
   const void* M; long long ldm; int m_bf16;
@@ -323,7 +330,7 @@ struct OrthSmem {
 template <int R>
 __device__ void reduce_gram(const double* __restrict__ part, int ngp, double* S) {
   constexpr int NP = npairs(R);
-  for (int q = threadIdx.x; q < NP; q += NT) {
+  for (int q = threadIdx.x; q < NP; q += blockDim.x) {
     int a = 0, rem = q;
     while (rem >= R - a) { rem -= R - a; a++; }
     const int b = a + rem;
@@ -338,7 +345,7 @@ __device__ void reduce_gram(const double* __restrict__ part, int ngp, double* S)
 // at the first degenerate column and returns 1.  Uses all threads.
 template <int R>
 __device__ int chol_inplace(double* S, double* gdiag, double tau2, bool detect, int* flag) {
-  for (int x = threadIdx.x; x < R; x += NT) gdiag[x] = S[x * R + x];
+  for (int x = threadIdx.x; x < R; x += blockDim.x) gdiag[x] = S[x * R + x];
   if (threadIdx.x == 0) *flag = 0;
   __syncthreads();
   for (int j = 0; j < R; j++) {
@@ -350,10 +357,10 @@ __device__ int chol_inplace(double* S, double* gdiag, double tau2, bool detect, 
     __syncthreads();
     if (*flag) return 1;
     const double ljj = S[j * R + j];
-    for (int i = j + 1 + threadIdx.x; i < R; i += NT) S[i * R + j] /= ljj;
+    for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) S[i * R + j] /= ljj;
     __syncthreads();
     const int rem = R - 1 - j;
-    for (int x = threadIdx.x; x < rem * rem; x += NT) {
+    for (int x = threadIdx.x; x < rem * rem; x += blockDim.x) {
       const int i = j + 1 + x / rem, k = j + 1 + x % rem;
       if (k <= i) S[i * R + k] -= S[i * R + j] * S[k * R + j];
     }
@@ -366,7 +373,7 @@ __device__ int chol_inplace(double* S, double* gdiag, double tau2, bool detect, 
 // kappa_est = ||L||_F * ||L^-1||_F (>= cond_2(L) = cond_2(P)).
 template <int R>
 __device__ void tri_inverse(const double* S, double* Li, double* kappa_out) {
-  for (int c = threadIdx.x; c < R; c += NT) {
+  for (int c = threadIdx.x; c < R; c += blockDim.x) {
     for (int i = 0; i < R; i++) Li[i * R + c] = 0.0;
     for (int i = c; i < R; i++) {
       double v = (i == c) ? 1.0 : 0.0;
@@ -425,12 +432,12 @@ template <int R>
 __device__ void apply_rinv(const float* src, float* dst, int r0, int nr, const double* Li,
                            const int* rep, bool use_rep, unsigned long long seed, float* ps) {
   __syncthreads();
-  for (int x = threadIdx.x; x < nr * R; x += NT) {
+  for (int x = threadIdx.x; x < nr * R; x += blockDim.x) {
     const int i = x / R, b = x % R;
     ps[x] = (use_rep && rep[b]) ? fallback_entry(seed, b, r0 + i) : __ldcg(src + (size_t)r0 * R + x);
   }
   __syncthreads();
-  for (int x = threadIdx.x; x < nr * R; x += NT) {
+  for (int x = threadIdx.x; x < nr * R; x += blockDim.x) {
     const int i = x / R, a = x % R;
     double v = 0.0;
     for (int b = 0; b <= a; b++) v = fma((double)ps[i * R + b], Li[a * R + b], v);
@@ -444,9 +451,9 @@ template <int R>
 __device__ void gram_partial(const float* src, int r0, int nr, double* part_u, float* ps) {
   constexpr int NP = npairs(R);
   __syncthreads();
-  for (int x = threadIdx.x; x < nr * R; x += NT) ps[x] = __ldcg(src + (size_t)r0 * R + x);
+  for (int x = threadIdx.x; x < nr * R; x += blockDim.x) ps[x] = __ldcg(src + (size_t)r0 * R + x);
   __syncthreads();
-  for (int q = threadIdx.x; q < NP; q += NT) {
+  for (int q = threadIdx.x; q < NP; q += blockDim.x) {
     int a = 0, rem = q;
     while (rem >= R - a) { rem -= R - a; a++; }
     const int b = a + rem;

@@ -19,6 +19,8 @@ __global__ void __launch_bounds__(NT) occ_step_kernel(Params p, int ph0, int ph1
   float* sm = reinterpret_cast<float*>(smraw);
   unsigned nb = 0;
   auto bar = [&]() { nb++; grid_barrier(p.bar, nb * gridDim.x); };
+  const bool stamp = coop && blockIdx.x == 0 && threadIdx.x == 0;
+  if (stamp) p.stats->t_ns[0] = gtimer();
   for (int ph = ph0; ph < ph1; ph++) {
     switch (ph) {
       case P_A: phase_A<R>(p, sm); break;
@@ -58,6 +60,7 @@ __global__ void __launch_bounds__(NT) occ_step_kernel(Params p, int ph0, int ph1
       default: break;
     }
     if (ph + 1 < ph1) bar();
+    if (stamp && ph + 1 < 12) p.stats->t_ns[ph + 1] = gtimer();
   }
   if (coop) {
     __syncthreads();
@@ -131,6 +134,8 @@ WsLayout make_layout(const Geometry& g, int nmat) {
   L.p_bucket = off; off = al(off + (size_t)nmat * g.n * R * 4);
   L.qw_bucket = off; off = al(off + (size_t)nmat * g.m * R * 4);
   L.qs_bucket = off; off = al(off + (size_t)nmat * g.m * R * 4);
+  L.v2_tail_bytes = nmat == 1 ? v2_tail_bytes(g.n, g.m, R, 148) : 0;
+  L.v2_tail = off; off = al(off + L.v2_tail_bytes);
   L.total = off;
   return L;
 }

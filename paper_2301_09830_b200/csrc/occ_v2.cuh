@@ -1,0 +1,177 @@
+// occ_v2.cuh -- the fused single-GPU step, TMEM-resident version (sm_100a).
+//
+// One persistent CTA per SM owns one tile (H rows x W cols, W wide enough
+// that one tile row is a >= 2-4 KB contiguous segment) for the whole step:
+//
+//  phase 1  cp.async.bulk streams the tile's rows of M and e, 8 rows per
+//           stage, into a padded staging ring (mbarrier complete_tx).  A = M+e
+//           (a1) is formed in registers; P^T_rows = Q_prev^T A^T_rows (a2) runs
+//           on the tensor cores (mma.sync m16n8k8 tf32, 3-term hi/lo split =
+//           fp32 accuracy), warps splitting the columns; A is stored in TENSOR
+//           MEMORY (tcgen05.st) in the per-lane fragment layout phases 3 and 5
+//           consume, so M and e are read from HBM exactly once.
+//  barrier  (P partials of the row band visible)
+//  phase 2  P_band = sum of the nc column-tile partials; the band's Gram
+//           partial P_band^T P_band in fp64 (a4).
+//  barrier
+//  phase 3  G = sum of the nr band partials; warp-level Cholesky in fp64 with
+//           the degenerate-column fallback (reading C3; slow paths add
+//           barriers); P_hat_band = P_band L^-T (a4); Q_part = A^T P_hat (a5)
+//           from TMEM on the tensor cores, complete per column group.
+//  barrier
+//  phase 4  Q = sum of the nr row-band partials, distributed over the CTAs of
+//           the column band, written to the output Q (a5, a9).
+//  barrier
+//  phase 5  M'^T = Q P_hat^T on the tensor cores (a7) in the same fragments
+//           as A in TMEM, e_new = A - round(M') (a8); stores M' and e_new.
+//
+// Fragment bookkeeping.  A tile is cut into cells of 8 rows x 16 cols; warp
+// w owns the column groups cg = w (mod 16) and every cell in them.  In a
+// cell at (r0, c0) lane (g = lane/4, t = lane%4) owns the four elements
+//   A[r0+2t][c0+g], A[r0+2t+1][c0+g], A[r0+2t][c0+g+8], A[r0+2t+1][c0+g+8]
+// which are (i) the B-operand registers of two m16n8k8 MMAs computing
+// Q^T += P_hat^T A over that cell when the k-index t maps to row 2t and t+4
+// to row 2t+1, and (ii) the accumulator registers of the m16n8k8 MMA
+// computing M'^T[c0..c0+16][r0..r0+8] = Q P_hat^T.  The four values live in
+// four TMEM columns of the warp's lanes (slot = rblk * CGW + cg / 16).
+#pragma once
+#include "occ_kernels.cuh"
+
+namespace occ {
+namespace v2 {
+
+constexpr int NT = 512;
+constexpr int NW = 16;
+constexpr int SR = 8;           // tile rows per staging stage (one cell row block)
+constexpr int MAX_STAGES = 4;
+constexpr int TMEM_CELLS = 32;  // cells per warp in TMEM (128 columns / 4)
+
+struct Params2 {
+  const void* M; long long ldm;
+  const float* err_in; long long lde_in;
+  float* err_out; long long lde_out;
+  void* recon; long long ldr;
+  int n, m;
+  const float* Qprev;  // m x R
+  float* Pout;         // n x R (P_hat)
+  float* Qout;         // m x R (Q)
+  int nr, nc, H, W;    // tile grid / tile shape
+  int ns, sw;          // staging stages, staging row stride (floats)
+  // shared-memory carve (bytes)
+  int off_stm, off_ste, off_qs, off_red, off_pa, off_pb, off_orth, off_ps, off_gs, smem_total;
+  // workspace
+  float* P_part;       // [nc][n][R]
+  double* G_band;      // [nr][NP]
+  double* G2_band;     // [nr][NP]
+  double* XY_band;     // [nr][2 R R]
+  float* Q_part;       // [nr][m][R]
+  unsigned* bar;
+  DevStats* stats;
+  unsigned long long fb_seed;
+  double tau, kappa_thr;
+  int force_two_pass;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ unsigned tf32_rna(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void split3(float x, unsigned& hi, unsigned& lo) {
+  hi = tf32_rna(x);
+  lo = tf32_rna(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// d += A . B with fp32-level accuracy: A = ah + al, B = bh + bl, drop al.bl
+__device__ __forceinline__ void mma3(float (&d)[4], const unsigned (&ah)[4], const unsigned (&al)[4], unsigned bh0,
+                                     unsigned bh1, unsigned bl0, unsigned bl1) {
+  mma_tf32(d, al, bh0, bh1);
+  mma_tf32(d, ah, bl0, bl1);
+  mma_tf32(d, ah, bh0, bh1);
+}
+
+__device__ __forceinline__ void tmem_st4(unsigned taddr, float a, float b, float c, float d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(__float_as_uint(a)),
+               "r"(__float_as_uint(b)), "r"(__float_as_uint(c)), "r"(__float_as_uint(d))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(unsigned taddr, float (&v)[4]) {
+  unsigned a, b, c, d;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  v[0] = __uint_as_float(a); v[1] = __uint_as_float(b); v[2] = __uint_as_float(c); v[3] = __uint_as_float(d);
+}
+
+// ------------------------------------------------------------------ geometry helpers
+struct Tile {
+  int rb, cb, row0, col0, th, tw, nrblk, ncg, ncells;
+};
+__device__ __forceinline__ Tile tile_of(const Params2& p) {
+  Tile t;
+  t.rb = blockIdx.x / p.nc;
+  t.cb = blockIdx.x % p.nc;
+  t.row0 = t.rb * p.H;
+  t.col0 = t.cb * p.W;
+  t.th = max(0, min(p.H, p.n - t.row0));
+  t.tw = max(0, min(p.W, p.m - t.col0));
+  t.nrblk = (t.th + 7) / 8;
+  t.ncg = (t.tw + 15) / 16;
+  t.ncells = t.nrblk * t.ncg;
+  return t;
+}
+
+// A element (i, j) of the tile from global memory (non-resident cells).
+template <bool MBF>
+__device__ __forceinline__ float gA(const Params2& p, int gi, int gj) {
+  float v;
+  if (MBF) v = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.M)[(size_t)gi * p.ldm + gj]);
+  else v = __ldcg(reinterpret_cast<const float*>(p.M) + (size_t)gi * p.ldm + gj);
+  if (p.err_in) v += __ldcg(p.err_in + (size_t)gi * p.lde_in + gj);
+  return v;
+}
+
+// the 4 cell values of lane (g,t) for cell (rblk, cg): rows r=8 rblk + 2t (+1), cols 16 cg + g (+8)
+template <bool MBF>
+__device__ __forceinline__ void cell_from_global(const Params2& p, const Tile& T, int rblk, int cg, int g, int t,
+                                                 float (&v)[4]) {
+  const int r = 8 * rblk + 2 * t, c = 16 * cg + g;
+  const int gi = T.row0 + r, gj = T.col0 + c;
+  v[0] = (r < T.th && c < T.tw) ? gA<MBF>(p, gi, gj) : 0.f;
+  v[1] = (r + 1 < T.th && c < T.tw) ? gA<MBF>(p, gi + 1, gj) : 0.f;
+  v[2] = (r < T.th && c + 8 < T.tw) ? gA<MBF>(p, gi, gj + 8) : 0.f;
+  v[3] = (r + 1 < T.th && c + 8 < T.tw) ? gA<MBF>(p, gi + 1, gj + 8) : 0.f;
+}
+
+}  // namespace v2
+}  // namespace occ

@@ -34,7 +34,8 @@ class occ_mat(ctypes.Structure):
 
 class occ_stats(ctypes.Structure):
     _fields_ = [("fallback_columns", ctypes.c_int32), ("second_pass", ctypes.c_int32),
-                ("kappa_est", ctypes.c_double), ("path", ctypes.c_int32), ("grid", ctypes.c_int32)]
+                ("kappa_est", ctypes.c_double), ("path", ctypes.c_int32), ("grid", ctypes.c_int32),
+                ("t_ns", ctypes.c_uint64 * 12)]
 
 
 class OccError(RuntimeError):
@@ -196,7 +197,7 @@ def occ_read_stats(ws, stream=None) -> dict:
     st = occ_stats()
     _check(lib().occ_read_stats(ws.data_ptr(), ctypes.byref(st), _stream(stream)), "occ_read_stats")
     return {"fallback_columns": st.fallback_columns, "second_pass": st.second_pass,
-            "kappa_est": st.kappa_est, "path": st.path, "grid": st.grid}
+            "kappa_est": st.kappa_est, "path": st.path, "grid": st.grid, "t_ns": list(st.t_ns)}
 
 
 def occ_check_status(stream=None, comm: Optional["Comm"] = None):
