@@ -249,7 +249,7 @@ def main():
     value = world * n * m * 4 / (ms * 1e-3) / 1e9               # GB/s uncompressed, whole job
     ab = alg_bytes(n, m)
     achieved = ab / (ms * 1e-3) / 1e9
-    launches_per_step = 1 if res["stats"]["path"] == 1 else 9
+    launches_per_step = 1 if res["stats"]["path"] in (1, 3) else 9
     if dp:
         launches_per_step = 3
 
@@ -332,7 +332,7 @@ def main():
             "config": {"workload": WORKLOAD if not dp else WORKLOAD + f"; data-parallel allreduce of P and Q over {world} ranks",
                        "n": n, "m": m, "rank": RANK, "M_dtype": "f32",
                        "parallelism": f"dp{world}" if dp else "1gpu", "l2": "flushed before every step",
-                       "path": "fused persistent kernel" if res["stats"]["path"] == 1 else "per-phase launches"},
+                       "path": {1: "v1 fused persistent kernel", 3: "fused TMEM-resident persistent kernel"}.get(res["stats"]["path"], "per-phase launches")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                          "alg_bytes_per_launch": ab, "kernel": "occ_step_kernel (fused)" if not dp else "step (3 launches + 2 NCCL)"},

@@ -80,17 +80,15 @@ struct Params {
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  // bar.sync orders the CTA's writes before thread 0's gpu-scope release
+  // (the CUTLASS GenericBarrier pattern); the acquire load orders the reads after.
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
     unsigned v;
-    while (true) {
+    do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-      if (v >= target) break;
-      __nanosleep(20);
-    }
-    __threadfence();
+    } while (v < target);
   }
   __syncthreads();
 }

@@ -25,15 +25,16 @@
 //  phase 5  M'^T = Q P_hat^T on the tensor cores (a7) in the same fragments
 //           as A in TMEM, e_new = A - round(M') (a8); stores M' and e_new.
 //
-// Fragment bookkeeping.  A tile is cut into cells of 8 rows x 16 cols; warp
-// w owns the column groups cg = w (mod 16) and every cell in them.  In a
-// cell at (r0, c0) lane (g = lane/4, t = lane%4) owns the four elements
-//   A[r0+2t][c0+g], A[r0+2t+1][c0+g], A[r0+2t][c0+g+8], A[r0+2t+1][c0+g+8]
-// which are (i) the B-operand registers of two m16n8k8 MMAs computing
-// Q^T += P_hat^T A over that cell when the k-index t maps to row 2t and t+4
-// to row 2t+1, and (ii) the accumulator registers of the m16n8k8 MMA
-// computing M'^T[c0..c0+16][r0..r0+8] = Q P_hat^T.  The four values live in
-// four TMEM columns of the warp's lanes (slot = rblk * CGW + cg / 16).
+// Fragment bookkeeping.  A tile is cut into cells of 8 rows x 16 cols; compute
+// warp w owns the column groups cg = w (mod NCW) and every cell in them.  In
+// a cell at (r0, c0) lane (g = lane/4, t = lane%4) owns the four elements
+//   A[r0+t][c0+2g], A[r0+t+4][c0+2g], A[r0+t][c0+2g+1], A[r0+t+4][c0+2g+1]
+// which are (i) the B-operand registers of the two m16n8k8 MMAs computing
+// Q^T += P_hat^T A over that cell (even / odd columns), and (ii) the
+// accumulator registers of the m16n8k8 MMA computing M'^T = Q P_hat^T over
+// it (column index n <-> 2n / 2(n-8)+1, row index n <-> n/2 + 4(n&1); see
+// occ_v2_kernel.cuh).  The four values live in four TMEM columns of the
+// warp's lanes (slot = (cg / NCW) * nrblk + rblk).
 #pragma once
 #include "occ_kernels.cuh"
 
@@ -42,9 +43,10 @@ namespace v2 {
 
 constexpr int NT = 512;
 constexpr int NW = 16;
+constexpr int NCW = NW - 1;     // compute warps; warp NW-1 is the phase-1 copy producer
 constexpr int SR = 8;           // tile rows per staging stage (one cell row block)
 constexpr int MAX_STAGES = 4;
-constexpr int TMEM_CELLS = 32;  // cells per warp in TMEM (128 columns / 4)
+constexpr int TMEM_CELLS = 512 / (NW / 4) / 4;  // cells per warp in TMEM (its columns / 4)
 
 struct Params2 {
   const void* M; long long ldm;
@@ -80,6 +82,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   asm volatile(
@@ -133,6 +138,20 @@ __device__ __forceinline__ void tmem_ld4(unsigned taddr, float (&v)[4]) {
   v[0] = __uint_as_float(a); v[1] = __uint_as_float(b); v[2] = __uint_as_float(c); v[3] = __uint_as_float(d);
 }
 
+// four consecutive cells (16 TMEM columns) in one load
+__device__ __forceinline__ void tmem_ld16(unsigned taddr, float (&v)[16]) {
+  unsigned r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 16; q++) v[q] = __uint_as_float(r[q]);
+}
+
 // ------------------------------------------------------------------ geometry helpers
 struct Tile {
   int rb, cb, row0, col0, th, tw, nrblk, ncg, ncells;
@@ -165,12 +184,12 @@ __device__ __forceinline__ float gA(const Params2& p, int gi, int gj) {
 template <bool MBF>
 __device__ __forceinline__ void cell_from_global(const Params2& p, const Tile& T, int rblk, int cg, int g, int t,
                                                  float (&v)[4]) {
-  const int r = 8 * rblk + 2 * t, c = 16 * cg + g;
+  const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
   const int gi = T.row0 + r, gj = T.col0 + c;
   v[0] = (r < T.th && c < T.tw) ? gA<MBF>(p, gi, gj) : 0.f;
-  v[1] = (r + 1 < T.th && c < T.tw) ? gA<MBF>(p, gi + 1, gj) : 0.f;
-  v[2] = (r < T.th && c + 8 < T.tw) ? gA<MBF>(p, gi, gj + 8) : 0.f;
-  v[3] = (r + 1 < T.th && c + 8 < T.tw) ? gA<MBF>(p, gi + 1, gj + 8) : 0.f;
+  v[1] = (r + 4 < T.th && c < T.tw) ? gA<MBF>(p, gi + 4, gj) : 0.f;
+  v[2] = (r < T.th && c + 1 < T.tw) ? gA<MBF>(p, gi, gj + 1) : 0.f;
+  v[3] = (r + 4 < T.th && c + 1 < T.tw) ? gA<MBF>(p, gi + 4, gj + 1) : 0.f;
 }
 
 }  // namespace v2

@@ -1,0 +1,527 @@
+// occ_v2_kernel.cuh -- body of the fused TMEM-resident step kernel (included
+// once, by occ_v2.cu).  Design and fragment bookkeeping: occ_v2.cuh.
+//
+// Index permutations used below (legal because a contraction index, and the
+// row/column order of an MMA output, may be permuted as long as both operands
+// and the consumer of the result agree):
+//  * phase 1, P^T = Q^T A^T (K = tile columns): k-index t <-> column 2t and
+//    t+4 <-> 2t+1 of an 8-column k-step, so a lane's B-operand pair is one
+//    8-byte shared load;
+//  * the cell layout (phases 1/3/5): lane (g,t) owns rows {t, t+4} x columns
+//    {2g, 2g+1} of the 8 x 16 cell, so phase-3 K (rows) is the identity map,
+//    phase-3/5 column n <-> 2n (n < 8), 2(n-8)+1 (n >= 8), phase-5 N (rows)
+//    n <-> n/2 + 4 (n & 1), and phase-5 stores are 8-byte pairs.
+#pragma once
+
+template <int R, bool MBF>
+__global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
+  constexpr int RP = K<R>::RP, MT = K<R>::MT, KS5 = K<R>::KS5, NP = K<R>::NP;
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ uint64_t mbar[2 * MAX_STAGES];   // full[], empty[]
+  __shared__ unsigned tmem_base_sh;
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const Tile T = tile_of(p);
+  const bool active = T.rb < p.nr && T.th > 0 && T.tw > 0;
+  unsigned nb = 0;
+  auto gbar = [&]() { nb++; grid_barrier(p.bar, nb * gridDim.x); };
+  const bool stamp = blockIdx.x == 0 && tid == 0;
+  if (stamp) p.stats->t_ns[0] = gtimer();
+
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < MAX_STAGES; s++) {
+      mbar_init(&mbar[s], 1);                      // full: the producer's expect_tx arrival
+      mbar_init(&mbar[MAX_STAGES + s], NCW);       // empty: one arrival per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tbase = tmem_base_sh;
+  // TMEM: warp w reaches lanes 32 (w % 4) ..; the warps sharing a lane quadrant split its 512 columns
+  const unsigned taddr_w = tbase + ((unsigned)((w & 3) * 32) << 16) + (unsigned)((w >> 2) * (512 / (NW / 4)));
+  // TMEM slot of a cell: column-group major, so one column group's cells are contiguous
+  auto cell_slot = [&](int rblk, int cg) { return (cg / NCW) * T.nrblk + rblk; };
+  auto consumer_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory"); };
+
+  // ============================================================== phase 1
+  unsigned char* stM = sm + p.off_stm;
+  float* stE = reinterpret_cast<float*>(sm + p.off_ste);  // e, then A = M + e
+  float* qs = reinterpret_cast<float*>(sm + p.off_qs);    // [W][RP] Q_prev slice (r > 16)
+  float* red = reinterpret_cast<float*>(sm + p.off_red);  // [NCW][nrblk][8][RP] per-warp P partials
+  const int nst = active ? T.nrblk : 0;
+  const size_t esz = MBF ? 2 : 4;
+  uint64_t* full = mbar;
+  uint64_t* empty = mbar + MAX_STAGES;
+  const int sw = p.sw;
+  auto issue = [&](int s) {
+    const int slot = s % p.ns;
+    const int r0 = s * SR, nrow = min(SR, T.th - r0);
+    const unsigned rbM = (unsigned)(T.tw * esz), rbE = (unsigned)(T.tw * 4);
+    mbar_expect_tx(&full[slot], (unsigned)nrow * (rbM + (p.err_in ? rbE : 0u)));
+    for (int i = 0; i < nrow; i++) {
+      const size_t gi = (size_t)(T.row0 + r0 + i);
+      bulk_g2s(stM + ((size_t)(slot * SR + i) * sw) * 4,
+               reinterpret_cast<const char*>(p.M) + (gi * p.ldm + T.col0) * esz, rbM, &full[slot]);
+      if (p.err_in)
+        bulk_g2s(stE + (size_t)(slot * SR + i) * sw, p.err_in + gi * p.lde_in + T.col0, rbE, &full[slot]);
+    }
+  };
+  // Q_prev^T fragments (A operand, 3-term split) of this warp's k-steps
+  constexpr bool QREG = (R <= 16);
+  constexpr int KREG = QREG ? (R <= 8 ? 8 : 4) : 1;
+  const int nk = T.tw / 8;
+  unsigned qf[KREG][MT][8];
+  auto qfrag = [&](const float* src, int ld, int c, int mt, unsigned (&f)[8]) {
+    const int k0 = 16 * mt + g;
+    const float* r0 = src + (size_t)(c + 2 * t) * ld;
+    const float* r1 = r0 + ld;
+    const float v0 = (k0 < R) ? r0[k0] : 0.f;
+    const float v1 = (k0 + 8 < R) ? r0[k0 + 8] : 0.f;
+    const float v2 = (k0 < R) ? r1[k0] : 0.f;
+    const float v3 = (k0 + 8 < R) ? r1[k0 + 8] : 0.f;
+    split3(v0, f[0], f[4]); split3(v1, f[1], f[5]); split3(v2, f[2], f[6]); split3(v3, f[3], f[7]);
+  };
+  unsigned long long wait_ns = 0;
+  if (w == NW - 1) {
+    // ---------------- producer
+    if (active && lane == 0) {
+      for (int s = 0; s < nst; s++) {
+        const int slot = s % p.ns;
+        if (s >= p.ns) mbar_wait(&empty[slot], (unsigned)(((s / p.ns) - 1) & 1));
+        issue(s);
+      }
+    }
+  } else {
+    // ---------------- consumers
+    if (active) {
+      if constexpr (QREG) {
+#pragma unroll
+        for (int j = 0; j < KREG; j++) {
+          const int kk = w + NCW * j;
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++) {
+            if (kk < nk) qfrag(p.Qprev + (size_t)T.col0 * R, R, 8 * kk, mt, qf[j][mt]);
+            else for (int q = 0; q < 8; q++) qf[j][mt][q] = 0u;
+          }
+        }
+      } else {
+        for (int x = tid; x < T.tw * RP; x += NCW * 32) {
+          const int c = x / RP, k = x % RP;
+          qs[x] = (k < R) ? __ldcg(p.Qprev + (size_t)(T.col0 + c) * R + k) : 0.f;
+        }
+        consumer_sync();
+      }
+    }
+    if (stamp) p.stats->t_ns[7] = gtimer();
+    const bool has_e = p.err_in != nullptr;
+    for (int s = 0; s < nst; s++) {
+      const int slot = s % p.ns;
+      const unsigned long long tw0 = stamp ? gtimer() : 0;
+      mbar_wait(&full[slot], (unsigned)((s / p.ns) & 1));
+      if (stamp) wait_ns += gtimer() - tw0;
+      const int nrow = min(SR, T.th - s * SR);
+      const unsigned char* sMb = stM + (size_t)slot * SR * sw * 4;
+      const float* sEb = stE + (size_t)slot * SR * sw;
+      // A[i][j..j+1] = M + e (two elements; rows >= nrow read as 0).  No CTA-wide
+      // sync per stage: every warp reads exactly the elements it consumes.
+      auto A2 = [&](int i, int j) -> float2 {
+        float2 a;
+        if (MBF) {
+          a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sMb + ((size_t)i * sw * 4 + (size_t)j * 2)));
+        } else {
+          a = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(sMb) + (size_t)i * sw + j);
+        }
+        if (has_e) {
+          const float2 e = *reinterpret_cast<const float2*>(sEb + (size_t)i * sw + j);
+          a.x += e.x; a.y += e.y;
+        }
+        return i < nrow ? a : make_float2(0.f, 0.f);
+      };
+      // (a) P^T[k][rows] = Q_prev^T[k][cols] A^T[cols][rows]; warps split the column k-steps,
+      //     one accumulator chain per k-step (independent MMA chains)
+      float acc[KREG][MT][4];
+#pragma unroll
+      for (int j = 0; j < KREG; j++)
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) acc[j][mt][0] = acc[j][mt][1] = acc[j][mt][2] = acc[j][mt][3] = 0.f;
+      if constexpr (QREG) {
+#pragma unroll
+        for (int j = 0; j < KREG; j++) {
+          const int kk = w + NCW * j;
+          if (kk < nk) {
+            const float2 b = A2(g, 8 * kk + 2 * t);
+            unsigned bh0, bl0, bh1, bl1;
+            split3(b.x, bh0, bl0);
+            split3(b.y, bh1, bl1);
+#pragma unroll
+            for (int mt = 0; mt < MT; mt++) {
+              const unsigned ah[4] = {qf[j][mt][0], qf[j][mt][1], qf[j][mt][2], qf[j][mt][3]};
+              const unsigned al[4] = {qf[j][mt][4], qf[j][mt][5], qf[j][mt][6], qf[j][mt][7]};
+              mma3(acc[j][mt], ah, al, bh0, bh1, bl0, bl1);
+            }
+          }
+        }
+      } else {
+        for (int kk = w; kk < nk; kk += NCW) {
+          const float2 b = A2(g, 8 * kk + 2 * t);
+          unsigned bh0, bl0, bh1, bl1;
+          split3(b.x, bh0, bl0);
+          split3(b.y, bh1, bl1);
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++) {
+            unsigned f[8];
+            qfrag(qs, RP, 8 * kk, mt, f);
+            const unsigned ah[4] = {f[0], f[1], f[2], f[3]}, al[4] = {f[4], f[5], f[6], f[7]};
+            mma3(acc[0][mt], ah, al, bh0, bh1, bl0, bl1);
+          }
+        }
+      }
+      // (b) TMEM: cells of row block s in this warp's column groups
+      for (int cg = w; cg < T.ncg; cg += NCW) {
+        const int cs = cell_slot(s, cg);
+        if (cs >= TMEM_CELLS) continue;
+        const int c = 16 * cg + 2 * g;
+        const bool ok = c < T.tw;   // tw is a multiple of 8, so c + 1 < tw too
+        const float2 x0 = ok ? A2(t, c) : make_float2(0.f, 0.f);
+        const float2 x1 = ok ? A2(t + 4, c) : make_float2(0.f, 0.f);
+        tmem_st4(taddr_w + (unsigned)(cs * 4), x0.x, x1.x, x0.y, x1.y);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);   // this warp is done with the slot
+      {  // this warp's partial P^T for rows 8s..8s+7 -> its own slot (reduced once after the loop)
+         // D[k][row]: c0 = (k=16mt+g, row=2t), c1 = (g, 2t+1), c2 = (g+8, 2t), c3 = (g+8, 2t+1)
+        float* rw = red + ((size_t)w * nst + s) * SR * RP;
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+          for (int j = 0; j < KREG; j++) { a0 += acc[j][mt][0]; a1 += acc[j][mt][1]; a2 += acc[j][mt][2]; a3 += acc[j][mt][3]; }
+          const int k0 = 16 * mt + g;
+          rw[(2 * t) * RP + k0] = a0;
+          rw[(2 * t + 1) * RP + k0] = a1;
+          if (k0 + 8 < RP) {
+            rw[(2 * t) * RP + k0 + 8] = a2;
+            rw[(2 * t + 1) * RP + k0 + 8] = a3;
+          }
+        }
+      }
+    }
+    consumer_sync();
+    // P_part rows of this tile: sum of the NCW warp partials (fixed order)
+    for (int x = tid; x < T.th * R; x += NCW * 32) {
+      const int i = x / R, k = x % R;
+      const float* rr = red + (size_t)i * RP + k;   // row i = stage i/8, row-in-stage i%8
+      float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < NCW; ww++) {
+        const float q = rr[(size_t)ww * nst * SR * RP];
+        if (ww & 1) v1 += q; else v0 += q;
+      }
+      p.P_part[((size_t)T.cb * p.n + T.row0 + i) * R + k] = v0 + v1;
+    }
+  }
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  if (stamp) p.stats->t_ns[8] = wait_ns;
+  gbar();
+  if (stamp) p.stats->t_ns[1] = gtimer();
+
+  // ============================================================== phase 2
+  const int H8 = T.nrblk * 8;
+  float* ps = reinterpret_cast<float*>(sm + p.off_ps);   // [H8][RP] P_band, later P_hat
+  float* ps2 = ps + (size_t)((p.H + 7) / 8 * 8) * RP;   // [H8][RP]
+  double* gscr = reinterpret_cast<double*>(sm + p.off_gs);
+  OrthW& o = *reinterpret_cast<OrthW*>(sm + p.off_orth);
+  if (active) {
+    for (int x = tid; x < H8 * RP; x += NT) {
+      const int i = x / RP, k = x % RP;
+      float v = 0.f;
+      if (i < T.th && k < R) {
+        const float* src = p.P_part + ((size_t)T.row0 + i) * R + k;
+        for (int c = 0; c < p.nc; c++) v += __ldcg(src + (size_t)c * p.n * R);
+      }
+      ps[x] = v;
+    }
+    __syncthreads();
+    if (T.cb == 0) band_gram<R>(ps, T.th, p.G_band + (size_t)T.rb * NP, gscr);
+  }
+  gbar();
+  if (stamp) p.stats->t_ns[2] = gtimer();
+
+  // ============================================================== phase 3
+  const double tau2 = p.tau * p.tau;
+  reduce_partials<R>(p.G_band, p.nr, o, gscr);
+  __syncthreads();
+  if (stamp) p.stats->t_ns[9] = gtimer();
+  if (w == 0) {
+    const int d = ldl_warp<R>(o, tau2, true);
+    if (lane == 0) o.deg = d;
+  }
+  __syncthreads();
+  if (stamp) p.stats->t_ns[10] = gtimer();
+  const bool deg = o.deg != 0;
+  if (deg) {  // slow path: augmented Gram with the fallback vector of every column
+    if (active && T.cb == 0) {
+      float* fs = ps2;
+      for (int x = tid; x < T.th * RP; x += NT) fs[x] = fallback_entry(p.fb_seed, x % RP, T.row0 + x / RP);
+      __syncthreads();
+      for (int q = tid; q < 2 * R * R; q += NT) {
+        const int which = q / (R * R), a = (q / R) % R, b = q % R;
+        const float* lhs = which ? fs : ps;
+        double gg = 0.0;
+        for (int i = 0; i < T.th; i++) gg = fma((double)lhs[i * RP + a], (double)fs[i * RP + b], gg);
+        p.XY_band[(size_t)T.rb * 2 * R * R + q] = gg;
+      }
+    }
+    gbar();
+    reduce_partials<R>(p.G_band, p.nr, o, gscr);
+    for (int q = tid; q < 2 * R * R; q += NT) {
+      double gg = 0.0;
+      for (int u = 0; u < p.nr; u++) gg += __ldcg(p.XY_band + (size_t)u * 2 * R * R + q);
+      const int a = (q / R) % R, b = q % R;
+      if (q < R * R) o.X[a * LD + b] = gg; else o.Y[a * LD + b] = gg;
+    }
+    __syncthreads();
+    ldl_subst<R>(o, tau2);
+  } else if (tid < 32) {
+    o.rep[tid] = 0;
+  }
+  __syncthreads();
+  if (w == 0) inverse_warp<R>(o);
+  __syncthreads();
+  const bool need2 = p.force_two_pass || o.kappa > p.kappa_thr;
+  if (stamp) p.stats->t_ns[11] = gtimer();
+  if (active) {
+    band_apply<R>(ps, ps2, T.th, o, deg, p.fb_seed, T.row0);
+    __syncthreads();
+    for (int x = tid; x < H8 * RP; x += NT) ps[x] = (x / RP < T.th) ? ps2[x] : 0.f;
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    int cnt = 0;
+    for (int j = 0; j < R; j++) cnt += deg ? o.rep[j] : 0;
+    p.stats->fallback_columns = cnt;
+    p.stats->second_pass = need2 ? 1 : 0;
+    p.stats->kappa_est = o.kappa;
+  }
+  if (need2) {  // CholQR2: orthonormalise the fp32-rounded P_hat once more
+    if (active && T.cb == 0) band_gram<R>(ps, T.th, p.G2_band + (size_t)T.rb * NP, gscr);
+    gbar();
+    reduce_partials<R>(p.G2_band, p.nr, o, gscr);
+    __syncthreads();
+    if (w == 0) ldl_warp<R>(o, 0.0, false);
+    __syncthreads();
+    if (w == 0) inverse_warp<R>(o);
+    __syncthreads();
+    if (active) {
+      band_apply<R>(ps, ps2, T.th, o, false, p.fb_seed, T.row0);
+      __syncthreads();
+      for (int x = tid; x < H8 * RP; x += NT) ps[x] = (x / RP < T.th) ? ps2[x] : 0.f;
+      __syncthreads();
+    }
+  }
+  if (stamp) p.stats->t_ns[3] = gtimer();
+  uint4* pa = reinterpret_cast<uint4*>(sm + p.off_pa);   // [nrblk][MT][32][2] (hi, lo)
+  uint4* pb = reinterpret_cast<uint4*>(sm + p.off_pb);   // [nrblk][KS5][32]   (h0, h1, l0, l1)
+  if (active) {
+    if (T.cb == 0)
+      for (int x = tid; x < T.th * R; x += NT) p.Pout[((size_t)T.row0 + x / R) * R + x % R] = ps[(x / R) * RP + x % R];
+    for (int x = tid; x < T.nrblk * MT * 32; x += NT) {   // phase-3 A operand: P_hat^T, K = rows t, t+4
+      const int ln = x % 32, mt = (x / 32) % MT, rblk = x / (32 * MT);
+      const int gg = ln >> 2, tt = ln & 3;
+      const int r0 = 8 * rblk + tt, k0 = 16 * mt + gg;
+      float v[4];
+      v[0] = (k0 < R) ? ps[r0 * RP + k0] : 0.f;
+      v[1] = (k0 + 8 < R) ? ps[r0 * RP + k0 + 8] : 0.f;
+      v[2] = (k0 < R) ? ps[(r0 + 4) * RP + k0] : 0.f;
+      v[3] = (k0 + 8 < R) ? ps[(r0 + 4) * RP + k0 + 8] : 0.f;
+      uint4 hi, lo;
+      split3(v[0], hi.x, lo.x); split3(v[1], hi.y, lo.y); split3(v[2], hi.z, lo.z); split3(v[3], hi.w, lo.w);
+      pa[2 * x] = hi;
+      pa[2 * x + 1] = lo;
+    }
+    for (int x = tid; x < T.nrblk * KS5 * 32; x += NT) {  // phase-5 B operand: P_hat^T, N = rows n/2 + 4(n&1)
+      const int ln = x % 32, ks = (x / 32) % KS5, rblk = x / (32 * KS5);
+      const int gg = ln >> 2, tt = ln & 3;
+      const int r = 8 * rblk + (gg >> 1) + 4 * (gg & 1), k = 8 * ks + tt;
+      uint4 v;
+      unsigned h0, l0, h1, l1;
+      split3((k < R) ? ps[r * RP + k] : 0.f, h0, l0);
+      split3((k + 4 < R) ? ps[r * RP + k + 4] : 0.f, h1, l1);
+      v.x = h0; v.y = h1; v.z = l0; v.w = l1;
+      pb[x] = v;
+    }
+  }
+  __syncthreads();
+  // phase 3a: Q_part[rb][cols] = A_tile^T P_hat_band, complete per column group in one warp
+  if (active) {
+    for (int cg = w; w < NCW && cg < T.ncg; cg += NCW) {
+      float qa[MT][2][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+        for (int nt = 0; nt < 2; nt++) qa[mt][nt][0] = qa[mt][nt][1] = qa[mt][nt][2] = qa[mt][nt][3] = 0.f;
+      for (int rb0 = 0; rb0 < T.nrblk; rb0 += 4) {
+        float v16[16];
+        const int cs0 = cell_slot(rb0, cg);
+        const bool batch = cs0 + 4 <= TMEM_CELLS;
+        if (batch) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          const int rblk = rb0 + jj;
+          if (rblk >= T.nrblk) break;
+          float v[4];
+          if (batch) { v[0] = v16[4 * jj]; v[1] = v16[4 * jj + 1]; v[2] = v16[4 * jj + 2]; v[3] = v16[4 * jj + 3]; }
+          else if (cs0 + jj < TMEM_CELLS) tmem_ld4(taddr_w + (unsigned)((cs0 + jj) * 4), v);
+          else cell_from_global<MBF>(p, T, rblk, cg, g, t, v);
+          unsigned vh[4], vl[4];
+#pragma unroll
+          for (int q = 0; q < 4; q++) split3(v[q], vh[q], vl[q]);
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++) {
+            const uint4 h = pa[2 * ((rblk * MT + mt) * 32 + lane)], l = pa[2 * ((rblk * MT + mt) * 32 + lane) + 1];
+            const unsigned ah[4] = {h.x, h.y, h.z, h.w}, al[4] = {l.x, l.y, l.z, l.w};
+            mma3(qa[mt][0], ah, al, vh[0], vh[1], vl[0], vl[1]);   // even columns 2g
+            mma3(qa[mt][1], ah, al, vh[2], vh[3], vl[2], vl[3]);   // odd columns 2g+1
+          }
+        }
+      }
+      // D[k][n]: c0 = (k=16mt+g, n=2t), c1 = (g, 2t+1), c2 = (g+8, 2t), c3 = (g+8, 2t+1); column = 2n + nt
+      float* dst = p.Q_part + ((size_t)T.rb * p.m + T.col0 + 16 * cg) * R;
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+        for (int nt = 0; nt < 2; nt++) {
+          const int col = 4 * t + nt, k = 16 * mt + g;
+          if (16 * cg + col < T.tw) {
+            if (k < R) dst[col * R + k] = qa[mt][nt][0];
+            if (k + 8 < R) dst[col * R + k + 8] = qa[mt][nt][2];
+          }
+          if (16 * cg + col + 2 < T.tw) {
+            if (k < R) dst[(col + 2) * R + k] = qa[mt][nt][1];
+            if (k + 8 < R) dst[(col + 2) * R + k + 8] = qa[mt][nt][3];
+          }
+        }
+    }
+  }
+  gbar();
+  if (stamp) p.stats->t_ns[4] = gtimer();
+
+  // ============================================================== phase 4
+  if (active) {
+    const int tot = T.tw * R;
+    const int per = (tot + p.nr - 1) / p.nr;
+    const int x0 = min(tot, T.rb * per), x1 = min(tot, x0 + per);
+    float* qscr = reinterpret_cast<float*>(gscr);
+    strided_sum<float>(p.Q_part + (size_t)T.col0 * R + x0, (size_t)p.m * R, p.nr, x1 - x0, qscr,
+                       [&](int e, float v) { p.Qout[(size_t)T.col0 * R + x0 + e] = v; });
+  }
+  gbar();
+  if (stamp) p.stats->t_ns[5] = gtimer();
+
+  // ============================================================== phase 5
+  if (active) {
+    for (int cg = w; w < NCW && cg < T.ncg; cg += NCW) {
+      unsigned qh[KS5][4], ql[KS5][4];
+      {  // A operand Q (M = columns 2g | 2g+1, K = rank)
+        const int cl = 16 * cg + 2 * g;
+        const bool okA = cl < T.tw, okB = cl + 1 < T.tw;
+        const float* qa_ = p.Qout + (size_t)(T.col0 + cl) * R;
+#pragma unroll
+        for (int ks = 0; ks < KS5; ks++) {
+          const int k0 = 8 * ks + t;
+          const float a0 = (okA && k0 < R) ? __ldcg(qa_ + k0) : 0.f;
+          const float a1 = (okB && k0 < R) ? __ldcg(qa_ + R + k0) : 0.f;
+          const float a2 = (okA && k0 + 4 < R) ? __ldcg(qa_ + k0 + 4) : 0.f;
+          const float a3 = (okB && k0 + 4 < R) ? __ldcg(qa_ + R + k0 + 4) : 0.f;
+          split3(a0, qh[ks][0], ql[ks][0]);
+          split3(a1, qh[ks][1], ql[ks][1]);
+          split3(a2, qh[ks][2], ql[ks][2]);
+          split3(a3, qh[ks][3], ql[ks][3]);
+        }
+      }
+      for (int rb0 = 0; rb0 < T.nrblk; rb0 += 4) {
+        float v16[16];
+        const int cs0 = cell_slot(rb0, cg);
+        const bool batch = cs0 + 4 <= TMEM_CELLS;
+        if (batch) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          const int rblk = rb0 + jj;
+          if (rblk >= T.nrblk) break;
+          float mr[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ks = 0; ks < KS5; ks++) {
+            const uint4 b = pb[(rblk * KS5 + ks) * 32 + lane];
+            mma3(mr, qh[ks], ql[ks], b.x, b.y, b.z, b.w);
+          }
+          float v[4];
+          if (batch) { v[0] = v16[4 * jj]; v[1] = v16[4 * jj + 1]; v[2] = v16[4 * jj + 2]; v[3] = v16[4 * jj + 3]; }
+          else if (cs0 + jj < TMEM_CELLS) tmem_ld4(taddr_w + (unsigned)((cs0 + jj) * 4), v);
+          else cell_from_global<MBF>(p, T, rblk, cg, g, t, v);
+          if (MBF) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) mr[q] = __bfloat162float(__float2bfloat16_rn(mr[q]));
+          }
+          // mr/v: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
+          const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
+          if (r + 4 < T.th && c + 1 < T.tw) {   // both rows and both columns inside: 8-byte pair stores
+            const size_t o0 = (size_t)(T.row0 + r) * p.ldr + (T.col0 + c);
+            if (p.recon) {
+              if (MBF) {
+                __nv_bfloat162* d0 = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + o0);
+                __nv_bfloat162* d1 = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + o0 + 4 * p.ldr);
+                *d0 = __floats2bfloat162_rn(mr[0], mr[2]);
+                *d1 = __floats2bfloat162_rn(mr[1], mr[3]);
+              } else {
+                float* d = reinterpret_cast<float*>(p.recon) + o0;
+                *reinterpret_cast<float2*>(d) = make_float2(mr[0], mr[2]);
+                *reinterpret_cast<float2*>(d + 4 * p.ldr) = make_float2(mr[1], mr[3]);
+              }
+            }
+            if (p.err_out) {
+              float* d = p.err_out + (size_t)(T.row0 + r) * p.lde_out + (T.col0 + c);
+              *reinterpret_cast<float2*>(d) = make_float2(v[0] - mr[0], v[2] - mr[2]);
+              *reinterpret_cast<float2*>(d + 4 * p.lde_out) = make_float2(v[1] - mr[1], v[3] - mr[3]);
+            }
+            continue;
+          }
+          const int rows[4] = {r, r + 4, r, r + 4}, cols[4] = {c, c, c + 1, c + 1};
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            if (rows[q] < T.th && cols[q] < T.tw) {
+              const size_t gi = (size_t)T.row0 + rows[q], gj = (size_t)T.col0 + cols[q];
+              if (p.recon) {
+                if (MBF) reinterpret_cast<__nv_bfloat16*>(p.recon)[gi * p.ldr + gj] = __float2bfloat16_rn(mr[q]);
+                else reinterpret_cast<float*>(p.recon)[gi * p.ldr + gj] = mr[q];
+              }
+              if (p.err_out) p.err_out[gi * p.lde_out + gj] = v[q] - mr[q];
+            }
+          }
+        }
+      }
+    }
+  }
+  if (stamp) p.stats->t_ns[6] = gtimer();
+
+  // ============================================================== teardown
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+  if (tid == 0) {
+    const unsigned old = atomicAdd(p.bar + 1, 1u);
+    if (old == gridDim.x - 1) {
+      atomicExch(p.bar, 0u);
+      atomicExch(p.bar + 1, 0u);
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    p.stats->path = 3;
+    p.stats->grid = gridDim.x;
+  }
+}

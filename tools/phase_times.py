@@ -18,10 +18,11 @@ def run(n, m, r, reps=20, bf16=False):
     P = torch.empty(n, r, device="cuda")
     R = torch.empty_like(M)
     ws = occ.alloc_workspace(n, m, r)
-    flush = torch.empty(64 * 1024 * 1024, device="cuda")
+    flush = torch.ones(64 * 1024 * 1024, device="cuda")
+    sink = torch.empty(1, device="cuda")
     acc = {}
     for i in range(reps):
-        flush.add_(1.0)
+        torch.sum(flush, dim=0, out=sink[0])   # clean read flush: no dirty lines left in L2
         occ.occ_compress(M, E, Q, P, R, r=r, ws=ws)
         torch.cuda.synchronize()
         st = occ.occ_read_stats(ws)
@@ -33,6 +34,13 @@ def run(n, m, r, reps=20, bf16=False):
         for a, b in zip(marks, marks[1:]):
             acc.setdefault(names[a], []).append((t[b] - t[a]) / 1e3)
         acc.setdefault("total", []).append((t[end] - t[0]) / 1e3)
+        if st["path"] == 3:
+            acc.setdefault("1.prologue", []).append((t[7] - t[0]) / 1e3)
+            acc.setdefault("1.wait_sum", []).append(t[8] / 1e3)
+            acc.setdefault("3.reduceG", []).append((t[9] - t[2]) / 1e3)
+            acc.setdefault("3.chol", []).append((t[10] - t[9]) / 1e3)
+            acc.setdefault("3.inverse", []).append((t[11] - t[10]) / 1e3)
+            acc.setdefault("3.apply", []).append((t[3] - t[11]) / 1e3)
     out = {k: sorted(v)[len(v) // 2] for k, v in acc.items()}
     print(json.dumps({"shape": [n, m, r], "bf16": bf16, "path": st["path"], "us": out, "grid": st["grid"]}))
 
