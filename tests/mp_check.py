@@ -1,0 +1,158 @@
+"""Multi-GPU parity check, run under torchrun (one rank per GPU, NCCL):
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tests/mp_check.py
+
+Checks, against the fp64 oracle simulating all ranks in-process:
+  * DP   occ_allreduce_factors over all ranks (local and global EF, reading C1/C2)
+  * PP   occ_send_factors (rank 1) -> occ_recv_factors (rank 0); the receiver's M'
+         must equal the sender's own decompression bit for bit (reading C8)
+  * EMB  occ_embed_sync dense (r = 0, reading C12) and compressed (r > 0, C14)
+Prints one JSON line per check on rank 0 and exits non-zero on any failure.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_2301_09830_b200 import occ  # noqa: E402
+from workloads import synth  # noqa: E402
+
+
+def rel(a, b, ref):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(ref), 1e-300))
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = occ.Comm.from_process_group()
+    assert comm.rank == rank and comm.nranks == world
+    ok = True
+
+    def report(name, **kw):
+        nonlocal ok
+        good = kw.pop("ok")
+        ok = ok and good
+        if rank == 0:
+            print(json.dumps({"check": name, "world": world, "ok": bool(good), **kw}), flush=True)
+
+    def gather_np(t):
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t.contiguous())
+        return [x.double().cpu().numpy() for x in out]
+
+    # ------------------------------------------------------------------ DP
+    for flags, name in ((0, "dp_local_ef"), (occ.OCC_EF_GLOBAL, "dp_global_ef")):
+        n, m, r = 768, 1024, 16
+        Ms = [synth.d2_gradlike(n, m, 500 + w) for w in range(world)]
+        Es = [synth.e0(n, m, 600 + w, like=Ms[w]) for w in range(world)]
+        Q0 = synth.q0(m, r, 7)
+        G = torch.from_numpy(Ms[rank]).to(dev)
+        E = torch.from_numpy(Es[rank]).to(dev)
+        Q = torch.from_numpy(Q0).to(dev)
+        P = torch.empty(n, r, device=dev)
+        occ.occ_allreduce_factors([G], [E], [Q], [P], r, 1.0 / world, flags=flags, comm=comm)
+        torch.cuda.synchronize()
+        o = oracle.dp_step(Ms, Es, Q0, scale=1.0 / world, ef_global=bool(flags & occ.OCC_EF_GLOBAL))
+        A = sum(Ms[w].astype(np.float64) + Es[w] for w in range(world))
+        gs, es = gather_np(G), gather_np(E)
+        e_recon = max(rel(gs[w], o["recon"], A / world) for w in range(world))
+        e_err = max(rel(es[w], o["err"][w], Ms[w].astype(np.float64) + Es[w]) for w in range(world))
+        same = all(np.array_equal(gs[0], gs[w]) for w in range(world))
+        orth = float(np.linalg.norm(P.double().cpu().numpy().T @ P.double().cpu().numpy() - np.eye(r)))
+        q_rel = rel(Q.double().cpu().numpy(), o["Q"], o["Q"])
+        report(name, recon_rel=e_recon, err_rel=e_err, q_rel=q_rel, orth=orth, identical_on_ranks=same,
+               ok=e_recon <= 1e-4 and e_err <= 1e-4 and same and orth <= 1e-5 and q_rel <= 1e-3)
+
+    # ------------------------------------------------------------------ PP (pairs 1 -> 0, 3 -> 2, ...)
+    if world >= 2:
+        n, m, r = 2048, 3072, 32      # BASELINE configs[2] shape class (8.3B hidden), shortened rows
+        sender = rank % 2 == 1
+        peer = rank - 1 if sender else rank + 1
+        pair = rank // 2
+        M = synth.d2_gradlike(n, m, 700 + pair)
+        E0 = synth.e0(n, m, 800 + pair, like=M)
+        Q0 = synth.q0(m, r, 9)
+        if peer < world:
+            if sender:
+                Md, Ed, Qd = (torch.from_numpy(x).to(dev) for x in (M, E0, Q0))
+                Pd = torch.empty(n, r, device=dev)
+                occ.occ_send_factors(Md, Ed, Qd, Pd, r, peer, comm)
+                own = torch.empty(n, m, device=dev)
+                occ.occ_decompress(Pd, Qd, own)          # what the sender's residual assumes
+                torch.cuda.synchronize()
+                dist.send(own, peer)
+                dist.send(Ed, peer)
+            else:
+                out = torch.empty(n, m, device=dev)
+                Pr = torch.empty(n, r, device=dev)
+                Qr = torch.empty(m, r, device=dev)
+                occ.occ_recv_factors(out, Pr, Qr, r, peer, comm)
+                torch.cuda.synchronize()
+                own, e_snd = torch.empty(n, m, device=dev), torch.empty(n, m, device=dev)
+                dist.recv(own, peer)
+                dist.recv(e_snd, peer)
+                own, e_snd = own.cpu(), e_snd.cpu()
+                o = oracle.compress_step(M, E0, Q0)
+                A = M.astype(np.float64) + E0
+                got = out.double().cpu().numpy()
+                r_rel = rel(got, o["recon"], A)
+                bit = bool(torch.equal(out.cpu(), own))
+                ef = rel(got + e_snd.double().numpy(), A, A)   # sender's e_new + receiver's M' = A
+                good = r_rel <= 1e-4 and bit and ef <= 1e-6
+                flag = torch.tensor([1 if good else 0], device=dev)
+        flags_t = torch.tensor([1], device=dev)
+        if peer < world and not sender:
+            flags_t = flag
+        dist.all_reduce(flags_t, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            report("pp_send_recv", recon_rel=r_rel, bitwise_equal_to_sender=bit, ef_identity=ef,
+                   ok=bool(flags_t.item()))
+        else:
+            ok = ok and bool(flags_t.item())
+
+    # ------------------------------------------------------------------ EMB dense (fused, reading C12)
+    V, h = 4096, 1024
+    D = max(1, world // 2)
+    Gs = [synth.d5_embedding_sparse(V, h, 900 + w) if w < D else synth.d2_gradlike(V, h, 900 + w)
+          for w in range(world)]
+    G = torch.from_numpy(Gs[rank]).to(dev)
+    occ.occ_embed_sync(G, None, None, None, 0, 1.0 / D, comm)
+    torch.cuda.synchronize()
+    want = oracle.embed_sync_fused(Gs, D)
+    got = G.double().cpu().numpy()
+    e1 = rel(got, want, want)
+    report("emb_dense", rel=e1, ok=e1 <= 1e-6)
+
+    # ------------------------------------------------------------------ EMB compressed (r > 0)
+    r = 16
+    G = torch.from_numpy(Gs[rank]).to(dev)
+    E = torch.zeros(V, h, device=dev)
+    Q0 = synth.q0(h, r, 11)
+    Q = torch.from_numpy(Q0).to(dev)
+    P = torch.empty(V, r, device=dev)
+    occ.occ_embed_sync(G, E, Q, P, r, 1.0 / D, comm)
+    torch.cuda.synchronize()
+    o = oracle.dp_step(Gs, None, Q0, scale=1.0 / D)
+    A = sum(g.astype(np.float64) for g in Gs)
+    e2 = rel(G.double().cpu().numpy(), o["recon"], A / D)
+    report("emb_compressed", recon_rel=e2, ok=e2 <= 1e-4)
+
+    comm.destroy()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
