@@ -468,3 +468,11 @@ occ_status occ_read_stats(const void* ws, occ_stats* out, cudaStream_t stream) {
 }
 
 }  // extern "C"
+
+extern "C" occ_status occ_read_trace(const void* ws, uint64_t* out, int count, cudaStream_t stream) {
+  if (!ws || !out || count < 0) return fail(OCC_ERR_INVALID_ARG, "null ws/out");
+  const size_t words = std::min<size_t>((size_t)count, kTraceBytes / 8);
+  cudaError_t e = cudaMemcpyAsync(out, static_cast<const char*>(ws) + kTraceOffset, words * 8, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_read_trace");
+}

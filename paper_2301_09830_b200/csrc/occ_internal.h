@@ -16,6 +16,10 @@ struct Geometry {
   int ngp = 0;           // Gram partial count (units of 128 rows)
 };
 
+constexpr size_t kTraceOffset = 256;
+constexpr int kTraceSlots = 32;                           // per CTA: 16 clock64 + 16 globaltimer stamps
+constexpr size_t kTraceBytes = 160 * kTraceSlots * 8;     // up to 160 CTAs
+
 struct WsLayout {
   size_t bar = 0, p_part = 0, q_part = 0, g_part = 0, g2_part = 0, xy_part = 0;
   size_t p_bucket = 0, qw_bucket = 0, qs_bucket = 0, v2_tail = 0, v2_tail_bytes = 0, total = 0;

@@ -126,6 +126,7 @@ WsLayout make_layout(const Geometry& g, int nmat) {
   const size_t np = (size_t)R * (R + 1) / 2;
   size_t off = 0;
   L.bar = off; off += 256;                                 // bar[2], ctl[4], stats
+  off += kTraceBytes;                                      // per-CTA phase trace (occ_read_trace)
   L.p_part = off; off = al(off + (size_t)g.s1 * g.n * R * 4);
   L.q_part = off; off = al(off + (size_t)g.s2 * g.m * R * 4);
   L.g_part = off; off = al(off + (size_t)g.ngp * np * 8);
@@ -134,7 +135,7 @@ WsLayout make_layout(const Geometry& g, int nmat) {
   L.p_bucket = off; off = al(off + (size_t)nmat * g.n * R * 4);
   L.qw_bucket = off; off = al(off + (size_t)nmat * g.m * R * 4);
   L.qs_bucket = off; off = al(off + (size_t)nmat * g.m * R * 4);
-  L.v2_tail_bytes = nmat == 1 ? v2_tail_bytes(g.n, g.m, R, 148) : 0;
+  L.v2_tail_bytes = v2_tail_bytes(g.n, g.m, R, 148);   // reused by every matrix of a multi-matrix call
   L.v2_tail = off; off = al(off + L.v2_tail_bytes);
   L.total = off;
   return L;

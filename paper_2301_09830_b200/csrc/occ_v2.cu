@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace occ {
@@ -29,6 +30,7 @@ struct OrthW {  // small fp64 linear algebra in shared memory
   double gdiag[32];     // diag(G): each column's own squared norm (degeneracy test)
   double D[32];
   double col[32];       // per-step broadcast buffer
+  double dinv[32];      // D^-1/2
   int rep[32];
   int deg;
   double kappa;
@@ -83,6 +85,17 @@ __device__ void reduce_partials(const double* __restrict__ part, int nparts, Ort
   });
 }
 
+// 1/d for normal d > 0: MUFU reciprocal estimate + two Newton steps (full fp64
+// accuracy; roughly half the latency of the IEEE division on the LDL chain).
+__device__ __forceinline__ double rcp_fast(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Warp-level right-looking LDL^T of the Gram in o.L (R <= 32), square-root free
 // so the sequential chain per column is one fp64 reciprocal.  Lane i holds row
 // i in registers; column j is broadcast through o.col.  detect: stop at the
@@ -102,7 +115,7 @@ __device__ int ldl_warp(OrthW& o, double tau2, bool detect) {
     const double d = o.col[j];
     const double gj = o.gdiag[j];
     if (detect && (gj == 0.0 || !(d >= tau2 * gj))) { deg = 1; break; }
-    const double rinv = 1.0 / (d > 0.0 ? d : 1e-300);
+    const double rinv = rcp_fast(d > 0.0 ? d : 1e-300);
     const double lij = row[j] * rinv;
 #pragma unroll
     for (int k = j + 1; k < R; k++)
@@ -114,6 +127,7 @@ __device__ int ldl_warp(OrthW& o, double tau2, bool detect) {
   if (!deg && i < R) {
 #pragma unroll
     for (int k = 0; k < R; k++) o.L[i * LD + k] = (k <= i) ? row[k] : 0.0;
+    o.dinv[i] = 1.0 / sqrt(o.D[i]);
   }
   __syncwarp();
   return deg;
@@ -163,7 +177,7 @@ __device__ void inverse_warp(OrthW& o) {
 // the modified column set c_j = rep[j] ? f_j : p_j is read from o.L (P^T P),
 // o.X (P^T F) and o.Y (F^T F); a column failing the test is replaced once.
 template <int R>
-__device__ void ldl_subst(OrthW& o, double tau2) {
+__device__ __noinline__ void ldl_subst(OrthW& o, double tau2) {
   if (threadIdx.x != 0) return;
   double* Lt = o.Li;  // scratch; o.L keeps P^T P until the end
   for (int x = 0; x < 32 * LD; x++) Lt[x] = 0.0;
@@ -192,22 +206,32 @@ __device__ void ldl_subst(OrthW& o, double tau2) {
     }
   }
   for (int x = 0; x < 32 * LD; x++) o.L[x] = Lt[x];
+  for (int j = 0; j < R; j++) o.dinv[j] = 1.0 / sqrt(o.D[j]);
 }
 
-// out[i][a] = sum_{b<=a} Pm[i][b] Li[a][b]  (fp64, rounded to fp32); Pm[i][b] = rep[b] ? f_b : ps[i][b]
+// P_hat rows = D^-1/2 L^-1 P[i] by forward substitution with the unit lower
+// L of G = L D L^T (no explicit inverse on the critical path).  One thread
+// per row, threads [t0, blockDim) (warp 0 is busy with the kappa estimate).
+// On the slow path ps already holds P_m (substituted columns replaced by their
+// fallback vectors, orth_slow).  fp64, rounded to fp32.
 template <int R>
-__device__ void band_apply(const float* ps, float* out, int nr, const OrthW& o, bool use_rep,
-                           unsigned long long seed, int row0) {
+__device__ void band_solve(const float* ps, float* out, int nr, const OrthW& o, int t0) {
   constexpr int RP = K<R>::RP;
-  for (int x = threadIdx.x; x < nr * R; x += blockDim.x) {
-    const int i = x / R, a = x % R;
-    double v = 0.0;
-#pragma unroll 4
-    for (int b = 0; b <= a; b++) {
-      const double pv = (use_rep && o.rep[b]) ? (double)fallback_entry(seed, b, row0 + i) : (double)ps[i * RP + b];
-      v = fma(pv, o.Li[a * LD + b], v);
+  for (int i = (int)threadIdx.x - t0; i < nr && i >= 0; i += (int)blockDim.x - t0) {
+    double x[R];
+#pragma unroll
+    for (int a = 0; a < R; a++) {
+      double v0 = (double)ps[i * RP + a];
+      double v1 = 0.0;
+#pragma unroll
+      for (int b = 0; b < a; b++) {
+        if (b & 1) v1 = fma(-o.L[a * LD + b], x[b], v1);
+        else v0 = fma(-o.L[a * LD + b], x[b], v0);
+      }
+      x[a] = v0 + v1;
     }
-    out[i * RP + a] = (float)v;
+#pragma unroll
+    for (int a = 0; a < R; a++) out[i * RP + a] = (float)(x[a] * o.dinv[a]);
   }
 }
 
@@ -233,6 +257,70 @@ __device__ void band_gram(const float* ps, int nr, double* part, double* scratch
   }
 }
 
+// ------------------------------------------------------------------ cold paths
+// Out of line (see the kernel's phase 3): taken only when a column is
+// degenerate (reading C3) or the first pass is ill conditioned (reading C5).
+
+// Slow path of the degenerate-column test: every column's fallback vector
+// enters an augmented Gram (X = P^T F, Y = F^T F, one partial per row band,
+// one extra grid barrier), the up-looking LDL^T with substitution decides
+// which columns are replaced, and the band's P columns that are replaced are
+// overwritten with their fallback vectors (P_m), so the solve is the common one.
+template <int R>
+__device__ __noinline__ void orth_slow(const Params2& p, Tile T, OrthW& o, float* ps, float* ps2, double* gscr,
+                                       unsigned epoch, bool active) {
+  constexpr int RP = K<R>::RP;
+  const int tid = threadIdx.x;
+  if (active && T.cb == 0) {
+    float* fs = ps2;
+    for (int x = tid; x < T.th * RP; x += NT) fs[x] = fallback_entry(p.fb_seed, x % RP, T.row0 + x / RP);
+    __syncthreads();
+    for (int q = tid; q < 2 * R * R; q += NT) {
+      const int which = q / (R * R), a = (q / R) % R, b = q % R;
+      const float* lhs = which ? fs : ps;
+      double gg = 0.0;
+      for (int i = 0; i < T.th; i++) gg = fma((double)lhs[i * RP + a], (double)fs[i * RP + b], gg);
+      p.XY_band[(size_t)T.rb * 2 * R * R + q] = gg;
+    }
+  }
+  grid_barrier(p.bar, epoch * gridDim.x);
+  reduce_partials<R>(p.G_band, p.nr, o, gscr);
+  for (int q = tid; q < 2 * R * R; q += NT) {
+    double gg = 0.0;
+    for (int u = 0; u < p.nr; u++) gg += __ldcg(p.XY_band + (size_t)u * 2 * R * R + q);
+    const int a = (q / R) % R, b = q % R;
+    if (q < R * R) o.X[a * LD + b] = gg; else o.Y[a * LD + b] = gg;
+  }
+  __syncthreads();
+  ldl_subst<R>(o, p.tau * p.tau);
+  __syncthreads();
+  if (active) {
+    for (int x = tid; x < T.th * RP; x += NT) {
+      const int a = x % RP;
+      if (a < R && o.rep[a]) ps[x] = fallback_entry(p.fb_seed, a, T.row0 + x / RP);
+    }
+  }
+}
+
+// CholQR2 (reading C5): orthonormalise the fp32-rounded P_hat in ps once more.
+template <int R>
+__device__ __noinline__ void second_pass(const Params2& p, Tile T, OrthW& o, float* ps, float* ps2, double* gscr,
+                                         unsigned epoch, bool active) {
+  constexpr int RP = K<R>::RP, NP = K<R>::NP;
+  if (active && T.cb == 0) band_gram<R>(ps, T.th, p.G2_band + (size_t)T.rb * NP, gscr);
+  grid_barrier(p.bar, epoch * gridDim.x);
+  reduce_partials<R>(p.G2_band, p.nr, o, gscr);
+  __syncthreads();
+  if (threadIdx.x < 32) ldl_warp<R>(o, 0.0, false);
+  __syncthreads();
+  if (active) {
+    band_solve<R>(ps, ps2, T.th, o, 0);
+    __syncthreads();
+    for (int x = threadIdx.x; x < T.nrblk * 8 * RP; x += NT) ps[x] = (x / RP < T.th) ? ps2[x] : 0.f;
+  }
+  __syncthreads();
+}
+
 #include "occ_v2_kernel.cuh"
 
 // ------------------------------------------------------------------ host side
@@ -240,6 +328,7 @@ struct Plan2 {
   bool ok = false;
   int nr = 0, nc = 0, H = 0, W = 0, ns = 0, sw = 0;
   int off_stm = 0, off_ste = 0, off_qs = 0, off_red = 0, off_pa = 0, off_pb = 0, off_orth = 0, off_ps = 0, off_gs = 0;
+  int off_qsm = 0;
   int total = 0, cells_per_warp = 0;
   double cost = 0;
 };
@@ -295,6 +384,7 @@ static Plan2 plan_for(int64_t n, int64_t m, int sms, bool mbf) {
     pl.off_orth = off; off += al128((int)sizeof(OrthW));
     pl.off_pa = off; off += al128(nrblk * MT * 32 * 32);
     pl.off_pb = off; off += al128(nrblk * KS5 * 32 * 16);
+    pl.off_qsm = off; off += al128(W * R * 4);   // phase-5 Q slice
     pl.total = std::max(p1, off);
     if (pl.total > smem_cap) continue;
     const int cgw = (ncg + NCW - 1) / NCW;
@@ -325,6 +415,7 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
   p.nr = pl.nr; p.nc = pl.nc; p.H = pl.H; p.W = pl.W; p.ns = pl.ns; p.sw = pl.sw;
   p.off_stm = pl.off_stm; p.off_ste = pl.off_ste; p.off_qs = pl.off_qs; p.off_red = pl.off_red;
   p.off_pa = pl.off_pa; p.off_pb = pl.off_pb; p.off_orth = pl.off_orth; p.off_ps = pl.off_ps; p.off_gs = pl.off_gs;
+  p.off_qsm = pl.off_qsm;
   p.smem_total = pl.total;
   char* tail = static_cast<char*>(ws_tail);
   constexpr int NP = K<R>::NP;
@@ -336,11 +427,16 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
   p.G2_band = reinterpret_cast<double*>(take((size_t)pl.nr * NP * 8));
   p.XY_band = reinterpret_cast<double*>(take((size_t)pl.nr * 2 * R * R * 8));
   p.bar = p1.bar;
+  p.trace = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(p1.bar) + kTraceOffset);
   p.stats = p1.stats;
   p.fb_seed = p1.fb_seed;
   p.tau = p1.tau;
   p.kappa_thr = p1.kappa_thr;
   p.force_two_pass = p1.force_two_pass;
+  {
+    const char* dbg = getenv("OCC_V2_DEBUG");
+    p.debug = dbg ? atoi(dbg) : 0;
+  }
   auto kern = occ_v2_kernel<R, MBF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
   if (e != cudaSuccess) return e;
@@ -352,7 +448,7 @@ template <int R>
 static size_t tail_bytes(const Plan2& pl, int64_t n, int64_t m) {
   constexpr int NP = K<R>::NP;
   auto a = [](size_t b) { return (b + 255) / 256 * 256; };
-  return a((size_t)pl.nc * n * R * 4) + a((size_t)pl.nr * m * R * 4) + 2 * a((size_t)pl.nr * NP * 8) +
+  return a((size_t)pl.nc * n * R * 4) + a((size_t)pl.nr * m * R * 4) + a((size_t)pl.nr * NP * 8) + a((size_t)pl.nr * NP * 8) +
          a((size_t)pl.nr * 2 * R * R * 8);
 }
 

@@ -60,7 +60,7 @@ struct Params2 {
   int nr, nc, H, W;    // tile grid / tile shape
   int ns, sw;          // staging stages, staging row stride (floats)
   // shared-memory carve (bytes)
-  int off_stm, off_ste, off_qs, off_red, off_pa, off_pb, off_orth, off_ps, off_gs, smem_total;
+  int off_stm, off_ste, off_qs, off_red, off_pa, off_pb, off_orth, off_ps, off_gs, off_qsm, smem_total;
   // workspace
   float* P_part;       // [nc][n][R]
   double* G_band;      // [nr][NP]
@@ -68,10 +68,12 @@ struct Params2 {
   double* XY_band;     // [nr][2 R R]
   float* Q_part;       // [nr][m][R]
   unsigned* bar;
+  unsigned long long* trace;   // [grid][32]: clock64 stamps 0..15, globaltimer stamps 16..31
   DevStats* stats;
   unsigned long long fb_seed;
   double tau, kappa_thr;
   int force_two_pass;
+  int debug;           // bit 0: skip phase-1 compute (streaming floor measurement only)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -180,16 +182,47 @@ __device__ __forceinline__ float gA(const Params2& p, int gi, int gj) {
   return v;
 }
 
-// the 4 cell values of lane (g,t) for cell (rblk, cg): rows r=8 rblk + 2t (+1), cols 16 cg + g (+8)
+// Cold paths, kept out of line so the hot unrolled loops of phases 3a/5 stay
+// compact in the instruction stream (all 148 SMs fetch the same code at once).
+// Values travel as float4 (registers), never through local memory.
+//
+// The 4 values of lane (g,t) for cell (rblk, cg) (order (r,c), (r+4,c),
+// (r,c+1), (r+4,c+1), r = 8 rblk + t, c = 16 cg + 2g): from TMEM slot cs when
+// it is resident, else recomputed from M and e in global memory.
 template <bool MBF>
-__device__ __forceinline__ void cell_from_global(const Params2& p, const Tile& T, int rblk, int cg, int g, int t,
-                                                 float (&v)[4]) {
+__device__ __noinline__ float4 cell_slow(const Params2& p, const Tile T, unsigned taddr, int cs, int rblk, int cg,
+                                         int g, int t) {
+  if (cs < TMEM_CELLS) {
+    float v[4];
+    tmem_ld4(taddr + (unsigned)(cs * 4), v);
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
   const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
   const int gi = T.row0 + r, gj = T.col0 + c;
-  v[0] = (r < T.th && c < T.tw) ? gA<MBF>(p, gi, gj) : 0.f;
-  v[1] = (r + 4 < T.th && c < T.tw) ? gA<MBF>(p, gi + 4, gj) : 0.f;
-  v[2] = (r < T.th && c + 1 < T.tw) ? gA<MBF>(p, gi, gj + 1) : 0.f;
-  v[3] = (r + 4 < T.th && c + 1 < T.tw) ? gA<MBF>(p, gi + 4, gj + 1) : 0.f;
+  float4 v;
+  v.x = (r < T.th && c < T.tw) ? gA<MBF>(p, gi, gj) : 0.f;
+  v.y = (r + 4 < T.th && c < T.tw) ? gA<MBF>(p, gi + 4, gj) : 0.f;
+  v.z = (r < T.th && c + 1 < T.tw) ? gA<MBF>(p, gi, gj + 1) : 0.f;
+  v.w = (r + 4 < T.th && c + 1 < T.tw) ? gA<MBF>(p, gi + 4, gj + 1) : 0.f;
+  return v;
+}
+
+// phase-5 stores of a cell on the tile edge, element-wise and bounds-checked
+template <bool MBF>
+__device__ __noinline__ void store_cell_edge(const Params2& p, const Tile T, int r, int c, float4 mr4, float4 v4) {
+  const float mr[4] = {mr4.x, mr4.y, mr4.z, mr4.w}, v[4] = {v4.x, v4.y, v4.z, v4.w};
+  const int rows[4] = {r, r + 4, r, r + 4}, cols[4] = {c, c, c + 1, c + 1};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    if (rows[q] < T.th && cols[q] < T.tw) {
+      const size_t gi = (size_t)T.row0 + rows[q], gj = (size_t)T.col0 + cols[q];
+      if (p.recon) {
+        if (MBF) reinterpret_cast<__nv_bfloat16*>(p.recon)[gi * p.ldr + gj] = __float2bfloat16_rn(mr[q]);
+        else reinterpret_cast<float*>(p.recon)[gi * p.ldr + gj] = mr[q];
+      }
+      if (p.err_out) p.err_out[gi * p.lde_out + gj] = v[q] - mr[q];
+    }
+  }
 }
 
 }  // namespace v2

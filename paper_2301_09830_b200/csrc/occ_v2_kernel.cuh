@@ -14,7 +14,7 @@
 #pragma once
 
 template <int R, bool MBF>
-__global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
+__global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ Params2 p) {
   constexpr int RP = K<R>::RP, MT = K<R>::MT, KS5 = K<R>::KS5, NP = K<R>::NP;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ uint64_t mbar[2 * MAX_STAGES];   // full[], empty[]
@@ -27,6 +27,13 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
   auto gbar = [&]() { nb++; grid_barrier(p.bar, nb * gridDim.x); };
   const bool stamp = blockIdx.x == 0 && tid == 0;
   if (stamp) p.stats->t_ns[0] = gtimer();
+  auto tr = [&](int k) {   // per-CTA phase trace (occ_read_trace)
+    if (tid == 0) {
+      p.trace[blockIdx.x * 32 + k] = clock64();
+      p.trace[blockIdx.x * 32 + 16 + k] = gtimer();
+    }
+  };
+  tr(0);
 
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
@@ -48,6 +55,15 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
   // TMEM slot of a cell: column-group major, so one column group's cells are contiguous
   auto cell_slot = [&](int rblk, int cg) { return (cg / NCW) * T.nrblk + rblk; };
   auto consumer_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory"); };
+  // four cells of a column group that are not all TMEM-resident (rare: out-of-line per cell)
+  auto fetch_slow = [&](int rb0, int cg, int cs0, float (&v16)[16]) {
+#pragma unroll
+    for (int jj = 0; jj < 4; jj++) {
+      const float4 c4 = (rb0 + jj < T.nrblk) ? cell_slow<MBF>(p, T, taddr_w, cs0 + jj, rb0 + jj, cg, g, t)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      v16[4 * jj] = c4.x; v16[4 * jj + 1] = c4.y; v16[4 * jj + 2] = c4.z; v16[4 * jj + 3] = c4.w;
+    }
+  };
 
   // ============================================================== phase 1
   unsigned char* stM = sm + p.off_stm;
@@ -126,6 +142,11 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
       mbar_wait(&full[slot], (unsigned)((s / p.ns) & 1));
       if (stamp) wait_ns += gtimer() - tw0;
       const int nrow = min(SR, T.th - s * SR);
+      if (p.debug & 1) {   // streaming-floor experiment: consume the slot without computing
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        continue;
+      }
       const unsigned char* sMb = stM + (size_t)slot * SR * sw * 4;
       const float* sEb = stE + (size_t)slot * SR * sw;
       // A[i][j..j+1] = M + e (two elements; rows >= nrow read as 0).  No CTA-wide
@@ -228,7 +249,9 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   if (stamp) p.stats->t_ns[8] = wait_ns;
+  tr(1);
   gbar();
+  tr(2);
   if (stamp) p.stats->t_ns[1] = gtimer();
 
   // ============================================================== phase 2
@@ -248,84 +271,60 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
       ps[x] = v;
     }
     __syncthreads();
+    // the band's Gram partial (one per row band: nr partials to reduce in phase 3)
     if (T.cb == 0) band_gram<R>(ps, T.th, p.G_band + (size_t)T.rb * NP, gscr);
   }
+  tr(3);
   gbar();
+  tr(4);
   if (stamp) p.stats->t_ns[2] = gtimer();
 
   // ============================================================== phase 3
-  const double tau2 = p.tau * p.tau;
+  // The hot path is one compact instruction stream; the rare branches (degenerate
+  // columns, CholQR2 pass) are out-of-line functions (cold code costs a memory
+  // round trip per fetch miss).
   reduce_partials<R>(p.G_band, p.nr, o, gscr);
   __syncthreads();
   if (stamp) p.stats->t_ns[9] = gtimer();
   if (w == 0) {
-    const int d = ldl_warp<R>(o, tau2, true);
+    const int d = ldl_warp<R>(o, p.tau * p.tau, true);
     if (lane == 0) o.deg = d;
   }
   __syncthreads();
   if (stamp) p.stats->t_ns[10] = gtimer();
   const bool deg = o.deg != 0;
-  if (deg) {  // slow path: augmented Gram with the fallback vector of every column
-    if (active && T.cb == 0) {
-      float* fs = ps2;
-      for (int x = tid; x < T.th * RP; x += NT) fs[x] = fallback_entry(p.fb_seed, x % RP, T.row0 + x / RP);
-      __syncthreads();
-      for (int q = tid; q < 2 * R * R; q += NT) {
-        const int which = q / (R * R), a = (q / R) % R, b = q % R;
-        const float* lhs = which ? fs : ps;
-        double gg = 0.0;
-        for (int i = 0; i < T.th; i++) gg = fma((double)lhs[i * RP + a], (double)fs[i * RP + b], gg);
-        p.XY_band[(size_t)T.rb * 2 * R * R + q] = gg;
-      }
-    }
-    gbar();
-    reduce_partials<R>(p.G_band, p.nr, o, gscr);
-    for (int q = tid; q < 2 * R * R; q += NT) {
-      double gg = 0.0;
-      for (int u = 0; u < p.nr; u++) gg += __ldcg(p.XY_band + (size_t)u * 2 * R * R + q);
-      const int a = (q / R) % R, b = q % R;
-      if (q < R * R) o.X[a * LD + b] = gg; else o.Y[a * LD + b] = gg;
-    }
-    __syncthreads();
-    ldl_subst<R>(o, tau2);
+  if (deg) {
+    nb++;
+    orth_slow<R>(p, T, o, ps, ps2, gscr, nb, active);
   } else if (tid < 32) {
     o.rep[tid] = 0;
   }
   __syncthreads();
+  tr(5);
+  // warp 0: kappa estimate (explicit inverse); warps 1..: P_hat rows by forward substitution
   if (w == 0) inverse_warp<R>(o);
+  else if (active) band_solve<R>(ps, ps2, T.th, o, 32);
   __syncthreads();
+  tr(12);
   const bool need2 = p.force_two_pass || o.kappa > p.kappa_thr;
   if (stamp) p.stats->t_ns[11] = gtimer();
   if (active) {
-    band_apply<R>(ps, ps2, T.th, o, deg, p.fb_seed, T.row0);
-    __syncthreads();
     for (int x = tid; x < H8 * RP; x += NT) ps[x] = (x / RP < T.th) ? ps2[x] : 0.f;
-    __syncthreads();
   }
   if (blockIdx.x == 0 && tid == 0) {
     int cnt = 0;
-    for (int j = 0; j < R; j++) cnt += deg ? o.rep[j] : 0;
+    for (int j = 0; j < R; j++) cnt += o.rep[j];
     p.stats->fallback_columns = cnt;
     p.stats->second_pass = need2 ? 1 : 0;
     p.stats->kappa_est = o.kappa;
   }
-  if (need2) {  // CholQR2: orthonormalise the fp32-rounded P_hat once more
-    if (active && T.cb == 0) band_gram<R>(ps, T.th, p.G2_band + (size_t)T.rb * NP, gscr);
-    gbar();
-    reduce_partials<R>(p.G2_band, p.nr, o, gscr);
-    __syncthreads();
-    if (w == 0) ldl_warp<R>(o, 0.0, false);
-    __syncthreads();
-    if (w == 0) inverse_warp<R>(o);
-    __syncthreads();
-    if (active) {
-      band_apply<R>(ps, ps2, T.th, o, false, p.fb_seed, T.row0);
-      __syncthreads();
-      for (int x = tid; x < H8 * RP; x += NT) ps[x] = (x / RP < T.th) ? ps2[x] : 0.f;
-      __syncthreads();
-    }
+  __syncthreads();
+  if (need2) {
+    nb++;
+    second_pass<R>(p, T, o, ps, ps2, gscr, nb, active);
   }
   if (stamp) p.stats->t_ns[3] = gtimer();
+  tr(13);
   uint4* pa = reinterpret_cast<uint4*>(sm + p.off_pa);   // [nrblk][MT][32][2] (hi, lo)
   uint4* pb = reinterpret_cast<uint4*>(sm + p.off_pb);   // [nrblk][KS5][32]   (h0, h1, l0, l1)
   if (active) {
@@ -358,27 +357,28 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
     }
   }
   __syncthreads();
+  tr(6);
   // phase 3a: Q_part[rb][cols] = A_tile^T P_hat_band, complete per column group in one warp
   if (active) {
     for (int cg = w; w < NCW && cg < T.ncg; cg += NCW) {
-      float qa[MT][2][4];
+      float qa2[2][MT][2][4];   // [row-block parity]: two independent accumulator chains
 #pragma unroll
-      for (int mt = 0; mt < MT; mt++)
+      for (int pr = 0; pr < 2; pr++)
 #pragma unroll
-        for (int nt = 0; nt < 2; nt++) qa[mt][nt][0] = qa[mt][nt][1] = qa[mt][nt][2] = qa[mt][nt][3] = 0.f;
+        for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+          for (int nt = 0; nt < 2; nt++) qa2[pr][mt][nt][0] = qa2[pr][mt][nt][1] = qa2[pr][mt][nt][2] = qa2[pr][mt][nt][3] = 0.f;
       for (int rb0 = 0; rb0 < T.nrblk; rb0 += 4) {
         float v16[16];
         const int cs0 = cell_slot(rb0, cg);
         const bool batch = cs0 + 4 <= TMEM_CELLS;
         if (batch) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
+        else fetch_slow(rb0, cg, cs0, v16);
 #pragma unroll
         for (int jj = 0; jj < 4; jj++) {
           const int rblk = rb0 + jj;
           if (rblk >= T.nrblk) break;
-          float v[4];
-          if (batch) { v[0] = v16[4 * jj]; v[1] = v16[4 * jj + 1]; v[2] = v16[4 * jj + 2]; v[3] = v16[4 * jj + 3]; }
-          else if (cs0 + jj < TMEM_CELLS) tmem_ld4(taddr_w + (unsigned)((cs0 + jj) * 4), v);
-          else cell_from_global<MBF>(p, T, rblk, cg, g, t, v);
+          const float v[4] = {v16[4 * jj], v16[4 * jj + 1], v16[4 * jj + 2], v16[4 * jj + 3]};
           unsigned vh[4], vl[4];
 #pragma unroll
           for (int q = 0; q < 4; q++) split3(v[q], vh[q], vl[q]);
@@ -386,11 +386,18 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
           for (int mt = 0; mt < MT; mt++) {
             const uint4 h = pa[2 * ((rblk * MT + mt) * 32 + lane)], l = pa[2 * ((rblk * MT + mt) * 32 + lane) + 1];
             const unsigned ah[4] = {h.x, h.y, h.z, h.w}, al[4] = {l.x, l.y, l.z, l.w};
-            mma3(qa[mt][0], ah, al, vh[0], vh[1], vl[0], vl[1]);   // even columns 2g
-            mma3(qa[mt][1], ah, al, vh[2], vh[3], vl[2], vl[3]);   // odd columns 2g+1
+            mma3(qa2[jj & 1][mt][0], ah, al, vh[0], vh[1], vl[0], vl[1]);   // even columns 2g
+            mma3(qa2[jj & 1][mt][1], ah, al, vh[2], vh[3], vl[2], vl[3]);   // odd columns 2g+1
           }
         }
       }
+      float qa[MT][2][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+        for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) qa[mt][nt][q] = qa2[0][mt][nt][q] + qa2[1][mt][nt][q];
       // D[k][n]: c0 = (k=16mt+g, n=2t), c1 = (g, 2t+1), c2 = (g+8, 2t), c3 = (g+8, 2t+1); column = 2n + nt
       float* dst = p.Q_part + ((size_t)T.rb * p.m + T.col0 + 16 * cg) * R;
 #pragma unroll
@@ -409,7 +416,9 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
         }
     }
   }
+  tr(7);
   gbar();
+  tr(8);
   if (stamp) p.stats->t_ns[4] = gtimer();
 
   // ============================================================== phase 4
@@ -421,24 +430,31 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
     strided_sum<float>(p.Q_part + (size_t)T.col0 * R + x0, (size_t)p.m * R, p.nr, x1 - x0, qscr,
                        [&](int e, float v) { p.Qout[(size_t)T.col0 * R + x0 + e] = v; });
   }
+  tr(9);
   gbar();
+  tr(10);
   if (stamp) p.stats->t_ns[5] = gtimer();
 
   // ============================================================== phase 5
+  float* qsm = reinterpret_cast<float*>(sm + p.off_qsm);   // [tw][R] Q of this tile's columns
+  if (active) {
+    for (int x = tid; x < T.tw * R; x += NT) qsm[x] = __ldcg(p.Qout + (size_t)T.col0 * R + x);
+  }
+  __syncthreads();
   if (active) {
     for (int cg = w; w < NCW && cg < T.ncg; cg += NCW) {
       unsigned qh[KS5][4], ql[KS5][4];
       {  // A operand Q (M = columns 2g | 2g+1, K = rank)
         const int cl = 16 * cg + 2 * g;
         const bool okA = cl < T.tw, okB = cl + 1 < T.tw;
-        const float* qa_ = p.Qout + (size_t)(T.col0 + cl) * R;
+        const float* qa_ = qsm + (size_t)cl * R;
 #pragma unroll
         for (int ks = 0; ks < KS5; ks++) {
           const int k0 = 8 * ks + t;
-          const float a0 = (okA && k0 < R) ? __ldcg(qa_ + k0) : 0.f;
-          const float a1 = (okB && k0 < R) ? __ldcg(qa_ + R + k0) : 0.f;
-          const float a2 = (okA && k0 + 4 < R) ? __ldcg(qa_ + k0 + 4) : 0.f;
-          const float a3 = (okB && k0 + 4 < R) ? __ldcg(qa_ + R + k0 + 4) : 0.f;
+          const float a0 = (okA && k0 < R) ? qa_[k0] : 0.f;
+          const float a1 = (okB && k0 < R) ? qa_[R + k0] : 0.f;
+          const float a2 = (okA && k0 + 4 < R) ? qa_[k0 + 4] : 0.f;
+          const float a3 = (okB && k0 + 4 < R) ? qa_[R + k0 + 4] : 0.f;
           split3(a0, qh[ks][0], ql[ks][0]);
           split3(a1, qh[ks][1], ql[ks][1]);
           split3(a2, qh[ks][2], ql[ks][2]);
@@ -450,20 +466,24 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
         const int cs0 = cell_slot(rb0, cg);
         const bool batch = cs0 + 4 <= TMEM_CELLS;
         if (batch) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
+        else fetch_slow(rb0, cg, cs0, v16);
+        float mr4[4][4];   // four cells, four independent MMA chains
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) mr4[jj][0] = mr4[jj][1] = mr4[jj][2] = mr4[jj][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < KS5; ks++)
+#pragma unroll
+          for (int jj = 0; jj < 4; jj++) {
+            const int rblk = min(rb0 + jj, T.nrblk - 1);
+            const uint4 b = pb[(rblk * KS5 + ks) * 32 + lane];
+            mma3(mr4[jj], qh[ks], ql[ks], b.x, b.y, b.z, b.w);
+          }
 #pragma unroll
         for (int jj = 0; jj < 4; jj++) {
           const int rblk = rb0 + jj;
           if (rblk >= T.nrblk) break;
-          float mr[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int ks = 0; ks < KS5; ks++) {
-            const uint4 b = pb[(rblk * KS5 + ks) * 32 + lane];
-            mma3(mr, qh[ks], ql[ks], b.x, b.y, b.z, b.w);
-          }
-          float v[4];
-          if (batch) { v[0] = v16[4 * jj]; v[1] = v16[4 * jj + 1]; v[2] = v16[4 * jj + 2]; v[3] = v16[4 * jj + 3]; }
-          else if (cs0 + jj < TMEM_CELLS) tmem_ld4(taddr_w + (unsigned)((cs0 + jj) * 4), v);
-          else cell_from_global<MBF>(p, T, rblk, cg, g, t, v);
+          float* mr = mr4[jj];
+          const float v[4] = {v16[4 * jj], v16[4 * jj + 1], v16[4 * jj + 2], v16[4 * jj + 3]};
           if (MBF) {
 #pragma unroll
             for (int q = 0; q < 4; q++) mr[q] = __bfloat162float(__float2bfloat16_rn(mr[q]));
@@ -491,23 +511,13 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(Params2 p) {
             }
             continue;
           }
-          const int rows[4] = {r, r + 4, r, r + 4}, cols[4] = {c, c, c + 1, c + 1};
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            if (rows[q] < T.th && cols[q] < T.tw) {
-              const size_t gi = (size_t)T.row0 + rows[q], gj = (size_t)T.col0 + cols[q];
-              if (p.recon) {
-                if (MBF) reinterpret_cast<__nv_bfloat16*>(p.recon)[gi * p.ldr + gj] = __float2bfloat16_rn(mr[q]);
-                else reinterpret_cast<float*>(p.recon)[gi * p.ldr + gj] = mr[q];
-              }
-              if (p.err_out) p.err_out[gi * p.lde_out + gj] = v[q] - mr[q];
-            }
-          }
+          store_cell_edge<MBF>(p, T, r, c, make_float4(mr[0], mr[1], mr[2], mr[3]), make_float4(v[0], v[1], v[2], v[3]));
         }
       }
     }
   }
   if (stamp) p.stats->t_ns[6] = gtimer();
+  tr(11);
 
   // ============================================================== teardown
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -79,6 +79,7 @@ def lib():
         "occ_comm_destroy": ([vp], c_int),
         "occ_check_status": ([vp, vp], c_int),
         "occ_read_stats": ([vp, ctypes.POINTER(occ_stats), vp], c_int),
+        "occ_read_trace": ([vp, ctypes.POINTER(ctypes.c_uint64), c_int, vp], c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

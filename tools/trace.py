@@ -1,0 +1,54 @@
+"""Per-CTA phase trace of the fused v2 kernel: work vs barrier wait, median / max over CTAs."""
+import os, sys, json, ctypes
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2301_09830_b200 import occ
+from workloads import synth
+
+SEG = [("phase1", 0, 1), ("B1 wait", 1, 2), ("phase2", 2, 3), ("B2 wait", 3, 4), ("reduceG+LDL+inv", 4, 5),
+       ("inv|solve", 5, 12), ("copy+need2", 12, 13), ("tables", 13, 6), ("phase3a", 6, 7), ("B3 wait", 7, 8), ("phase4", 8, 9), ("B4 wait", 9, 10),
+       ("phase5", 10, 11)]
+
+
+def run(n, m, r, reps=8):
+    M = torch.from_numpy(synth.d2_gradlike(n, m, 5)).cuda()
+    E = torch.from_numpy(synth.e0(n, m, 6, like=synth.d2_gradlike(64, 64, 1))).cuda()
+    Q = torch.from_numpy(synth.q0(m, r, 7)).cuda()
+    P = torch.empty(n, r, device="cuda")
+    R = torch.empty_like(M)
+    ws = occ.alloc_workspace(n, m, r)
+    flush = torch.ones(64 * 1024 * 1024, device="cuda")
+    sink = torch.empty(1, device="cuda")
+    buf = (ctypes.c_uint64 * (160 * 32))()
+    res = {}
+    for i in range(reps):
+        if not os.environ.get("NOFLUSH"):
+            torch.sum(flush, dim=0, out=sink[0])
+        occ.occ_compress(M, E, Q, P, R, r=r, ws=ws)
+        torch.cuda.synchronize()
+        assert occ.lib().occ_read_trace(ws.data_ptr(), buf, 160 * 32, None) == 0
+        st = occ.occ_read_stats(ws)
+        if i < 3:
+            continue
+        g = st["grid"]
+        tr = np.array(buf[: g * 32], dtype=np.float64).reshape(g, 32)
+        gt = tr[:, 16:]
+        ck = tr[:, :16]
+        t0 = gt[:, 0].min()
+        for name, a, b in SEG:
+            d = (gt[:, b] - gt[:, a]) / 1e3
+            res.setdefault(name, []).append((np.median(d), d.max()))
+            c = (ck[:, b] - ck[:, a]) / 1e3
+            res.setdefault(name + " [kclk]", []).append((np.median(c), c.max()))
+        res.setdefault("total(max end - min start)", []).append(((gt[:, 11].max() - t0) / 1e3,) * 2)
+        res.setdefault("start skew", []).append(((gt[:, 0].max() - t0) / 1e3,) * 2)
+    out = {k: {"median_us": round(float(np.median([x[0] for x in v])), 2), "max_us": round(float(np.median([x[1] for x in v])), 2)}
+           for k, v in res.items()}
+    print(json.dumps({"shape": [n, m, r], "grid": g, "second_pass": st["second_pass"], "kappa": st["kappa_est"], "fallback": st["fallback_columns"]}))
+    for k, v in out.items():
+        print(f"  {k:28s} median {v['median_us']:7.2f} us   max {v['max_us']:7.2f} us")
+
+
+if __name__ == "__main__":
+    for spec in sys.argv[1:] or ["4096x1920x16"]:
+        run(*map(int, spec.split("x")))
