@@ -92,9 +92,11 @@ typedef struct {
   int32_t fallback_columns; /* columns replaced by their deterministic fallback vector (reading C3) */
   int32_t second_pass;      /* 1 if the second CholQR pass ran */
   double kappa_est;         /* ||L||_F * ||L^-1||_F of the first Cholesky factor (>= cond_2(P)) */
-  int32_t path;             /* 1 = fused persistent kernel, 2 = one launch per phase */
+  int32_t path;             /* 1 = fused persistent kernel (v1), 2 = one launch per phase, 3 = TMEM-resident fused kernel (v2) */
   int32_t grid;             /* CTAs of the persistent kernel */
-  uint64_t t_ns[12];        /* fused path: %globaltimer when CTA 0 entered phase k (0 = A, 1 = B, 3 = C, 6 = D, 7 = E, 8 = F, 9 = end) */
+  uint64_t t_ns[12];        /* %globaltimer stamps of CTA 0 at phase boundaries (diagnostic) */
+  double q_amp;             /* v2: ||S Li^T||_F, the rounding amplification of the fused Q = (A^T P) Li^T; -1 if not computed */
+  int32_t q_fused;          /* v2: 1 if Q was formed as (A^T P) Li^T (reading C20), 0 if as A^T P_hat */
 } occ_stats;
 
 const char* occ_status_string(occ_status s);

@@ -464,6 +464,8 @@ occ_status occ_read_stats(const void* ws, occ_stats* out, cudaStream_t stream) {
   out->path = d.path;
   out->grid = d.grid;
   for (int k = 0; k < 12; k++) out->t_ns[k] = d.t_ns[k];
+  out->q_amp = d.q_amp;
+  out->q_fused = d.q_fused;
   return OCC_OK;
 }
 

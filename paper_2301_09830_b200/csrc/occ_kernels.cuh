@@ -40,6 +40,8 @@ struct DevStats {
   int path;
   int grid;
   unsigned long long t_ns[12];   // %globaltimer at phase boundaries (CTA 0)
+  double q_amp;                  // fused path: ||S Li^T||_F (-1: not computed)
+  int q_fused;                   // fused path: Q = (A^T P) Li^T was used
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

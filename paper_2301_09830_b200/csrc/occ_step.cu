@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(NT) occ_step_kernel(Params p, int ph0, int ph1
   if (blockIdx.x == 0 && threadIdx.x == 0 && ph0 <= P_F && P_F < ph1) {
     p.stats->path = p.path;
     p.stats->grid = gridDim.x;
+    p.stats->q_amp = -1.0;
+    p.stats->q_fused = 0;
   }
 }
 

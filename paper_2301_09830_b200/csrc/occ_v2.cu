@@ -1,6 +1,7 @@
 // occ_v2.cu -- kernel body and launcher of the TMEM-resident fused step
 // (design in occ_v2.cuh).
 #include "occ_v2.cuh"
+#include "occ_v2_la.cuh"
 #include "occ_internal.h"
 
 #include <algorithm>
@@ -11,251 +12,6 @@
 
 namespace occ {
 namespace v2 {
-
-template <int R>
-struct K {
-  static constexpr int RP = R < 8 ? 8 : R;   // padded rank
-  static constexpr int MT = (RP + 15) / 16;  // m-tiles of 16 over the rank
-  static constexpr int KS5 = RP / 8;         // phase-5 k-steps
-  static constexpr int NP = npairs(R);
-};
-
-constexpr int LD = 33;   // padded stride of the small fp64 matrices: conflict-free rows and columns
-
-struct OrthW {  // small fp64 linear algebra in shared memory
-  double L[32 * LD];    // Gram (full), then the unit lower factor of G = L D L^T
-  double Li[32 * LD];   // D^-1/2 L^-1: P_hat = P Li^T
-  double X[32 * LD];    // P^T F (slow path)
-  double Y[32 * LD];    // F^T F (slow path)
-  double gdiag[32];     // diag(G): each column's own squared norm (degeneracy test)
-  double D[32];
-  double col[32];       // per-step broadcast buffer
-  double dinv[32];      // D^-1/2
-  int rep[32];
-  int deg;
-  double kappa;
-};
-
-// out[e] = sum_{u < S} src[u * stride + e], e < E, in a fixed order (deterministic).
-// Every thread keeps 16 independent loads in flight: the partial sums live in
-// L2 and this is latency bound.  scratch: NT elements of shared memory.
-template <typename Tv, typename Fout>
-__device__ void strided_sum(const Tv* __restrict__ src, size_t stride, int S, int E, Tv* scratch, Fout&& out) {
-  for (int e0 = 0; e0 < E; e0 += NT) {
-    const int En = min(NT, E - e0);
-    const int C = max(1, NT / En);
-    const int x = threadIdx.x;
-    Tv acc = Tv(0);
-    if (x < En * C) {
-      const int e = e0 + x % En, c = x / En;
-      for (int u0 = c; u0 < S; u0 += 16 * C) {
-        Tv v[16];
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-          const int u = u0 + j * C;
-          v[j] = (u < S) ? __ldcg(src + (size_t)u * stride + e) : Tv(0);
-        }
-#pragma unroll
-        for (int j = 0; j < 16; j++) acc += v[j];
-      }
-    }
-    __syncthreads();
-    if (x < En * C) scratch[x] = acc;
-    __syncthreads();
-    if (x < En) {
-      Tv r = Tv(0);
-      for (int c = 0; c < C; c++) r += scratch[c * En + x];
-      out(e0 + x, r);
-    }
-    __syncthreads();
-  }
-}
-
-// G (packed upper triangle, nparts partials) -> o.L (full symmetric), o.gdiag.  All threads.
-template <int R>
-__device__ void reduce_partials(const double* __restrict__ part, int nparts, OrthW& o, double* scratch) {
-  constexpr int NP = K<R>::NP;
-  strided_sum<double>(part, NP, nparts, NP, scratch, [&](int q, double gsum) {
-    int a = 0, rem = q;
-    while (rem >= R - a) { rem -= R - a; a++; }
-    const int b = a + rem;
-    o.L[a * LD + b] = gsum;
-    o.L[b * LD + a] = gsum;
-    if (a == b) o.gdiag[a] = gsum;
-  });
-}
-
-// 1/d for normal d > 0: MUFU reciprocal estimate + two Newton steps (full fp64
-// accuracy; roughly half the latency of the IEEE division on the LDL chain).
-__device__ __forceinline__ double rcp_fast(double d) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  double e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  return fma(r, e, r);
-}
-
-// Warp-level right-looking LDL^T of the Gram in o.L (R <= 32), square-root free
-// so the sequential chain per column is one fp64 reciprocal.  Lane i holds row
-// i in registers; column j is broadcast through o.col.  detect: stop at the
-// first column whose squared residual D_j is below tau2 * its own squared norm
-// (reading C3: the MGS test ||v|| < tau ||p_j||) and return 1.  Warp 0 only.
-template <int R>
-__device__ int ldl_warp(OrthW& o, double tau2, bool detect) {
-  const int i = threadIdx.x & 31;
-  double row[R];
-#pragma unroll
-  for (int k = 0; k < R; k++) row[k] = (i < R) ? o.L[i * LD + k] : 0.0;
-  int deg = 0;
-#pragma unroll
-  for (int j = 0; j < R; j++) {
-    if (i >= j && i < R) o.col[i] = row[j];   // u_i = G_ij after the previous updates
-    __syncwarp();
-    const double d = o.col[j];
-    const double gj = o.gdiag[j];
-    if (detect && (gj == 0.0 || !(d >= tau2 * gj))) { deg = 1; break; }
-    const double rinv = rcp_fast(d > 0.0 ? d : 1e-300);
-    const double lij = row[j] * rinv;
-#pragma unroll
-    for (int k = j + 1; k < R; k++)
-      if (i >= k && i < R) row[k] = fma(-lij, o.col[k], row[k]);
-    if (i > j) row[j] = lij;
-    if (i == j) { o.D[j] = d; row[j] = 1.0; }
-    __syncwarp();
-  }
-  if (!deg && i < R) {
-#pragma unroll
-    for (int k = 0; k < R; k++) o.L[i * LD + k] = (k <= i) ? row[k] : 0.0;
-    o.dinv[i] = 1.0 / sqrt(o.D[i]);
-  }
-  __syncwarp();
-  return deg;
-}
-
-// o.Li = D^-1/2 L^-1 for the unit lower L; kappa = ||L D^1/2||_F ||D^-1/2 L^-1||_F
-// (>= cond_2(P)).  Warp 0; lane c owns column c of L^-1.
-template <int R>
-__device__ void inverse_warp(OrthW& o) {
-  const int c = threadIdx.x & 31;
-  double col[R];
-#pragma unroll
-  for (int i = 0; i < R; i++) {
-    double v0 = (i == c) ? 1.0 : 0.0, v1 = 0.0;   // two chains for ILP
-#pragma unroll
-    for (int k = 0; k < i; k++) {
-      if (k & 1) v1 = fma(-o.L[i * LD + k], col[k], v1);
-      else v0 = fma(-o.L[i * LD + k], col[k], v0);
-    }
-    col[i] = (i >= c && c < R) ? v0 + v1 : 0.0;
-  }
-  // D^-1/2 of every column, computed in parallel and broadcast through o.col
-  if (c < R) o.col[c] = 1.0 / sqrt(o.D[c] > 0.0 ? o.D[c] : 1e-300);
-  __syncwarp();
-  const double sdc = (c < R) ? sqrt(o.D[c] > 0.0 ? o.D[c] : 0.0) : 0.0;
-  double nl = 0.0, ni = 0.0;
-  if (c < R) {
-#pragma unroll
-    for (int i = 0; i < R; i++) {
-      const double v = col[i] * o.col[i];
-      o.Li[i * LD + c] = v;
-      ni = fma(v, v, ni);
-      const double lc = o.L[i * LD + c] * sdc;   // (L D^1/2)[i][c]
-      nl = fma(lc, lc, nl);
-    }
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    nl += __shfl_xor_sync(0xffffffffu, nl, off);
-    ni += __shfl_xor_sync(0xffffffffu, ni, off);
-  }
-  if (c == 0) o.kappa = sqrt(nl) * sqrt(ni);
-  __syncwarp();
-}
-
-// Up-looking LDL^T with column substitution (slow path, thread 0): the Gram of
-// the modified column set c_j = rep[j] ? f_j : p_j is read from o.L (P^T P),
-// o.X (P^T F) and o.Y (F^T F); a column failing the test is replaced once.
-template <int R>
-__device__ __noinline__ void ldl_subst(OrthW& o, double tau2) {
-  if (threadIdx.x != 0) return;
-  double* Lt = o.Li;  // scratch; o.L keeps P^T P until the end
-  for (int x = 0; x < 32 * LD; x++) Lt[x] = 0.0;
-  for (int j = 0; j < R; j++) o.rep[j] = 0;
-  auto gram = [&](int a, int b) -> double {
-    const bool ra = o.rep[a], rb = o.rep[b];
-    if (!ra && !rb) return o.L[a * LD + b];
-    if (!ra && rb) return o.X[a * LD + b];
-    if (ra && !rb) return o.X[b * LD + a];
-    return o.Y[a * LD + b];
-  };
-  for (int i = 0; i < R; i++) {
-    for (int attempt = 0; attempt < 2; attempt++) {
-      for (int k = 0; k < i; k++) {
-        double v = gram(i, k);
-        for (int l = 0; l < k; l++) v -= Lt[i * LD + l] * o.D[l] * Lt[k * LD + l];
-        Lt[i * LD + k] = v / o.D[k];
-      }
-      const double g = gram(i, i);
-      double d = g;
-      for (int k = 0; k < i; k++) d -= Lt[i * LD + k] * Lt[i * LD + k] * o.D[k];
-      if (attempt == 0 && (g == 0.0 || !(d >= tau2 * g))) { o.rep[i] = 1; continue; }
-      o.D[i] = d > 0.0 ? d : 1e-300;
-      Lt[i * LD + i] = 1.0;
-      break;
-    }
-  }
-  for (int x = 0; x < 32 * LD; x++) o.L[x] = Lt[x];
-  for (int j = 0; j < R; j++) o.dinv[j] = 1.0 / sqrt(o.D[j]);
-}
-
-// P_hat rows = D^-1/2 L^-1 P[i] by forward substitution with the unit lower
-// L of G = L D L^T (no explicit inverse on the critical path).  One thread
-// per row, threads [t0, blockDim) (warp 0 is busy with the kappa estimate).
-// On the slow path ps already holds P_m (substituted columns replaced by their
-// fallback vectors, orth_slow).  fp64, rounded to fp32.
-template <int R>
-__device__ void band_solve(const float* ps, float* out, int nr, const OrthW& o, int t0) {
-  constexpr int RP = K<R>::RP;
-  for (int i = (int)threadIdx.x - t0; i < nr && i >= 0; i += (int)blockDim.x - t0) {
-    double x[R];
-#pragma unroll
-    for (int a = 0; a < R; a++) {
-      double v0 = (double)ps[i * RP + a];
-      double v1 = 0.0;
-#pragma unroll
-      for (int b = 0; b < a; b++) {
-        if (b & 1) v1 = fma(-o.L[a * LD + b], x[b], v1);
-        else v0 = fma(-o.L[a * LD + b], x[b], v0);
-      }
-      x[a] = v0 + v1;
-    }
-#pragma unroll
-    for (int a = 0; a < R; a++) out[i * RP + a] = (float)(x[a] * o.dinv[a]);
-  }
-}
-
-// Gram partial (packed) of rows [0,nr) of an fp32 [.][RP] array, fp64.
-template <int R>
-__device__ void band_gram(const float* ps, int nr, double* part, double* scratch) {
-  constexpr int RP = K<R>::RP, NP = K<R>::NP;
-  const int gsz = max(1, (int)blockDim.x / NP);
-  for (int x = threadIdx.x; x < NP * gsz; x += blockDim.x) {
-    const int q = x % NP, grp = x / NP;
-    int a = 0, rem = q;
-    while (rem >= R - a) { rem -= R - a; a++; }
-    const int b = a + rem;
-    double gg = 0.0;
-    for (int i = grp; i < nr; i += gsz) gg = fma((double)ps[i * RP + a], (double)ps[i * RP + b], gg);
-    scratch[x] = gg;
-  }
-  __syncthreads();
-  for (int q = threadIdx.x; q < NP; q += blockDim.x) {
-    double gg = 0.0;
-    for (int grp = 0; grp < gsz; grp++) gg += scratch[grp * NP + q];
-    part[q] = gg;
-  }
-}
 
 // ------------------------------------------------------------------ cold paths
 // Out of line (see the kernel's phase 3): taken only when a column is
@@ -314,11 +70,149 @@ __device__ __noinline__ void second_pass(const Params2& p, Tile T, OrthW& o, flo
   if (threadIdx.x < 32) ldl_warp<R>(o, 0.0, false);
   __syncthreads();
   if (active) {
-    band_solve<R>(ps, ps2, T.th, o, 0);
+    band_solve<R>(ps, ps2, T.th, o, 0, NT);
     __syncthreads();
     for (int x = threadIdx.x; x < T.nrblk * 8 * RP; x += NT) ps[x] = (x / RP < T.th) ? ps2[x] : 0.f;
   }
   __syncthreads();
+}
+
+// Phase-3 A-operand table of an [H8][RP] factor band X (X^T, K = rows t, t+4),
+// 3-term split: pa[(rblk MT + mt) 32 + lane] = (hi, lo).  All threads.
+template <int R>
+__device__ __forceinline__ void build_pa(const float* X, int nrblk, uint4* pa) {
+  constexpr int RP = K<R>::RP, MT = K<R>::MT;
+  for (int x = threadIdx.x; x < nrblk * MT * 32; x += NT) {
+    const int ln = x % 32, mt = (x / 32) % MT, rblk = x / (32 * MT);
+    const int gg = ln >> 2, tt = ln & 3;
+    const int r0 = 8 * rblk + tt, k0 = 16 * mt + gg;
+    float v[4];
+    v[0] = (k0 < R) ? X[r0 * RP + k0] : 0.f;
+    v[1] = (k0 + 8 < R) ? X[r0 * RP + k0 + 8] : 0.f;
+    v[2] = (k0 < R) ? X[(r0 + 4) * RP + k0] : 0.f;
+    v[3] = (k0 + 8 < R) ? X[(r0 + 4) * RP + k0 + 8] : 0.f;
+    uint4 hi, lo;
+    split3(v[0], hi.x, lo.x); split3(v[1], hi.y, lo.y); split3(v[2], hi.z, lo.z); split3(v[3], hi.w, lo.w);
+    pa[2 * x] = hi;
+    pa[2 * x + 1] = lo;
+  }
+}
+
+// Four consecutive cells of a column group that are not all TMEM-resident.
+template <bool MBF>
+__device__ __forceinline__ void cells4_slow(const Params2& p, const Tile T, unsigned taddr_w, int rb0, int cg, int cs0,
+                                            int g, int t, float (&v16)[16]) {
+#pragma unroll
+  for (int jj = 0; jj < 4; jj++) {
+    const float4 c4 = (rb0 + jj < T.nrblk) ? cell_slow<MBF>(p, T, taddr_w, cs0 + jj, rb0 + jj, cg, g, t)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    v16[4 * jj] = c4.x; v16[4 * jj + 1] = c4.y; v16[4 * jj + 2] = c4.z; v16[4 * jj + 3] = c4.w;
+  }
+}
+
+// Q_part[rb][tile columns] = A_tile^T X_band on the tensor cores, A read from
+// TMEM, X^T from the pa table; complete per column group in one compute warp
+// (warps >= NCW return at once).
+template <int R, bool MBF>
+__device__ __forceinline__ void q_part_from_tmem(const Params2& p, const Tile T, const uint4* pa, unsigned taddr_w) {
+  constexpr int MT = K<R>::MT;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  for (int cg = w; w < NCW && cg < T.ncg; cg += NCW) {
+    float qa2[2][MT][2][4];   // [row-block parity]: two independent accumulator chains
+#pragma unroll
+    for (int pr = 0; pr < 2; pr++)
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+        for (int nt = 0; nt < 2; nt++) qa2[pr][mt][nt][0] = qa2[pr][mt][nt][1] = qa2[pr][mt][nt][2] = qa2[pr][mt][nt][3] = 0.f;
+    for (int rb0 = 0; rb0 < T.nrblk; rb0 += 4) {
+      float v16[16];
+      const int cs0 = (cg / NCW) * T.nrblk + rb0;   // TMEM cell slot (see the kernel)
+      if (cs0 + 4 <= TMEM_CELLS) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
+      else cells4_slow<MBF>(p, T, taddr_w, rb0, cg, cs0, g, t, v16);
+#pragma unroll
+      for (int jj = 0; jj < 4; jj++) {
+        const int rblk = rb0 + jj;
+        if (rblk >= T.nrblk) break;
+        unsigned vh[4], vl[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) split3(v16[4 * jj + q], vh[q], vl[q]);
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          const uint4 h = pa[2 * ((rblk * MT + mt) * 32 + lane)], l = pa[2 * ((rblk * MT + mt) * 32 + lane) + 1];
+          const unsigned ah[4] = {h.x, h.y, h.z, h.w}, al[4] = {l.x, l.y, l.z, l.w};
+          mma3(qa2[jj & 1][mt][0], ah, al, vh[0], vh[1], vl[0], vl[1]);   // even columns 2g
+          mma3(qa2[jj & 1][mt][1], ah, al, vh[2], vh[3], vl[2], vl[3]);   // odd columns 2g+1
+        }
+      }
+    }
+    // D[k][n]: c0 = (k=16mt+g, n=2t), c1 = (g, 2t+1), c2 = (g+8, 2t), c3 = (g+8, 2t+1); column = 2n + nt
+    float* dst = p.Q_part + ((size_t)T.rb * p.m + T.col0 + 16 * cg) * R;
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+      for (int nt = 0; nt < 2; nt++) {
+        float qa[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) qa[q] = qa2[0][mt][nt][q] + qa2[1][mt][nt][q];
+        const int col = 4 * t + nt, k = 16 * mt + g;
+        if (16 * cg + col < T.tw) {
+          if (k < R) dst[col * R + k] = qa[0];
+          if (k + 8 < R) dst[col * R + k + 8] = qa[2];
+        }
+        if (16 * cg + col + 2 < T.tw) {
+          if (k < R) dst[(col + 2) * R + k] = qa[1];
+          if (k + 8 < R) dst[(col + 2) * R + k + 8] = qa[3];
+        }
+      }
+  }
+}
+
+// Columns [c0, c1) of its tile whose Q this CTA reduces (row band rb of nr).
+__device__ __forceinline__ int2 q_slice(const Tile T, int nr) {
+  const int per = (T.tw + nr - 1) / nr;
+  const int c0 = min(T.tw, T.rb * per);
+  return make_int2(c0, min(T.tw, c0 + per));
+}
+
+// The general orthonormalisation + Q path (reading C3/C5, and whenever the fused
+// Q = (A^T P) Li^T would amplify rounding, see the kernel's phase 3): degenerate
+// columns, P_hat by forward substitution, the optional CholQR2 pass, then
+// Q_part = A^T P_hat from TMEM, one grid barrier, and the column-slice reduce
+// into Q.  P_hat is left in ps.  Returns the barrier epoch count.
+template <int R, bool MBF>
+__device__ __noinline__ unsigned cold_orth_q(const Params2& p, Tile T, OrthW& o, float* ps, float* ps2, double* gscr,
+                                             uint4* pa, unsigned taddr_w, unsigned nb, bool active, bool deg) {
+  constexpr int RP = K<R>::RP;
+  const int tid = threadIdx.x, w = tid >> 5;
+  if (deg) {
+    nb++;
+    orth_slow<R>(p, T, o, ps, ps2, gscr, nb, active);
+  }
+  __syncthreads();
+  if (w == NW - 1) inverse_warp<R>(o);
+  else if (active) band_solve<R>(ps, ps2, T.th, o, 0, NCW * 32);
+  __syncthreads();
+  const bool need2 = p.force_two_pass || o.kappa > p.kappa_thr;
+  if (active)
+    for (int x = tid; x < T.nrblk * 8 * RP; x += NT) ps[x] = (x / RP < T.th) ? ps2[x] : 0.f;
+  __syncthreads();
+  if (need2) {
+    nb++;
+    second_pass<R>(p, T, o, ps, ps2, gscr, nb, active);
+  }
+  if (active) build_pa<R>(ps, T.nrblk, pa);
+  __syncthreads();
+  if (active) q_part_from_tmem<R, MBF>(p, T, pa, taddr_w);
+  nb++;
+  grid_barrier(p.bar, nb * gridDim.x);
+  if (active) {
+    const int2 cs = q_slice(T, p.nr);
+    float* Qo = p.Qout + (size_t)(T.col0 + cs.x) * R;
+    strided_sum<float>(p.Q_part + (size_t)(T.col0 + cs.x) * R, (size_t)p.m * R, p.nr, (cs.y - cs.x) * R,
+                       reinterpret_cast<float*>(gscr), [&](int e, float v) { Qo[e] = v; });
+  }
+  return nb;
 }
 
 #include "occ_v2_kernel.cuh"
@@ -437,6 +331,11 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
     const char* dbg = getenv("OCC_V2_DEBUG");
     p.debug = dbg ? atoi(dbg) : 0;
   }
+  // fused-Q gate (reading C20): rounding of A^T P is amplified by at most ~amp;
+  // 32 keeps it well inside the 1e-4 parity budget.  Debug bit 2 forces the
+  // general path.
+  p.amp_thr = (p.debug & 4) ? -1.0 : 32.0;
+  p.spec = (pl.cells_per_warp <= TMEM_CELLS && !(p.debug & 16)) ? 1 : 0;
   auto kern = occ_v2_kernel<R, MBF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
   if (e != cudaSuccess) return e;

@@ -72,9 +72,28 @@ struct Params2 {
   DevStats* stats;
   unsigned long long fb_seed;
   double tau, kappa_thr;
+  double amp_thr;      // fused-Q gate on ||S Li^T||_F (phase 3)
+  int spec;            // every cell TMEM-resident: the fused result is checked after phase 5
   int force_two_pass;
   int debug;           // bit 0: skip phase-1 compute (streaming floor measurement only)
 };
+
+// ------------------------------------------------------------------ group grid barrier
+// grid_barrier over a sub-group of each CTA's threads (sync() is the group's
+// CTA-level barrier, thread 0 must belong to it): the CTA's other warps keep
+// working (phase 3: warp NW-1 finishes the conditioning estimates meanwhile).
+template <class Sync>
+__device__ __forceinline__ void grid_barrier_group(unsigned* ctr, unsigned target, Sync sync) {
+  sync();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  sync();
+}
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }

@@ -33,6 +33,12 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       p.trace[blockIdx.x * 32 + 16 + k] = gtimer();
     }
   };
+  auto trw = [&](int k) {   // stamp from lane 0 of the calling warp
+    if (lane == 0) {
+      p.trace[blockIdx.x * 32 + k] = clock64();
+      p.trace[blockIdx.x * 32 + 16 + k] = gtimer();
+    }
+  };
   tr(0);
 
   if (w == 0) {
@@ -55,15 +61,6 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   // TMEM slot of a cell: column-group major, so one column group's cells are contiguous
   auto cell_slot = [&](int rblk, int cg) { return (cg / NCW) * T.nrblk + rblk; };
   auto consumer_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory"); };
-  // four cells of a column group that are not all TMEM-resident (rare: out-of-line per cell)
-  auto fetch_slow = [&](int rb0, int cg, int cs0, float (&v16)[16]) {
-#pragma unroll
-    for (int jj = 0; jj < 4; jj++) {
-      const float4 c4 = (rb0 + jj < T.nrblk) ? cell_slow<MBF>(p, T, taddr_w, cs0 + jj, rb0 + jj, cg, g, t)
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-      v16[4 * jj] = c4.x; v16[4 * jj + 1] = c4.y; v16[4 * jj + 2] = c4.z; v16[4 * jj + 3] = c4.w;
-    }
-  };
 
   // ============================================================== phase 1
   unsigned char* stM = sm + p.off_stm;
@@ -255,11 +252,20 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (stamp) p.stats->t_ns[1] = gtimer();
 
   // ============================================================== phase 2
+  // P_band (sum of the band's nc column-tile partials); then, concurrently,
+  //   compute warps:  Q~_part = A_tile^T P_band   (tensor cores, A from TMEM)
+  //   warp NW-1:      the band's Gram partial P_band^T P_band (fp64, cb == 0)
+  // Q = A^T P_hat = (A^T P) Li^T with P_hat = P Li^T, Li = D^-1/2 L^-1 (reading
+  // C20), so the product with A needs no orthonormalised factor and leaves the
+  // critical path; Li is applied to the reduced Q~ in phase 3.
   const int H8 = T.nrblk * 8;
   float* ps = reinterpret_cast<float*>(sm + p.off_ps);   // [H8][RP] P_band, later P_hat
   float* ps2 = ps + (size_t)((p.H + 7) / 8 * 8) * RP;   // [H8][RP]
   double* gscr = reinterpret_cast<double*>(sm + p.off_gs);
   OrthW& o = *reinterpret_cast<OrthW*>(sm + p.off_orth);
+  uint4* pa = reinterpret_cast<uint4*>(sm + p.off_pa);   // [nrblk][MT][32][2] (hi, lo)
+  uint4* pb = reinterpret_cast<uint4*>(sm + p.off_pb);   // [nrblk][KS5][32]   (h0, h1, l0, l1)
+  float* qsm = reinterpret_cast<float*>(sm + p.off_qsm);   // phase 3: Q~ slice; phase 5: [tw][R] Q of the tile
   if (active) {
     for (int x = tid; x < H8 * RP; x += NT) {
       const int i = x / RP, k = x % RP;
@@ -271,8 +277,14 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       ps[x] = v;
     }
     __syncthreads();
-    // the band's Gram partial (one per row band: nr partials to reduce in phase 3)
-    if (T.cb == 0) band_gram<R>(ps, T.th, p.G_band + (size_t)T.rb * NP, gscr);
+    build_pa<R>(ps, T.nrblk, pa);
+    __syncthreads();
+    if (w == NW - 1) {
+      if (T.cb == 0) band_gram_warp<R>(ps, T.th, p.G_band + (size_t)T.rb * NP);
+      trw(14);
+    } else {
+      q_part_from_tmem<R, MBF>(p, T, pa, taddr_w);
+    }
   }
   tr(3);
   gbar();
@@ -280,244 +292,186 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (stamp) p.stats->t_ns[2] = gtimer();
 
   // ============================================================== phase 3
-  // The hot path is one compact instruction stream; the rare branches (degenerate
-  // columns, CholQR2 pass) are out-of-line functions (cold code costs a memory
-  // round trip per fetch miss).
+  // G = sum of the nr band partials (all threads); then warp NW-1 factors it
+  // (LDL^T with the degenerate-column test) while the compute warps reduce
+  // this CTA's column slice of Q~ over the nr row bands.
   reduce_partials<R>(p.G_band, p.nr, o, gscr);
-  __syncthreads();
+  tr(6);
   if (stamp) p.stats->t_ns[9] = gtimer();
-  if (w == 0) {
+  const int2 qs_cols = active ? q_slice(T, p.nr) : make_int2(0, 0);
+  const int nqc = qs_cols.y - qs_cols.x;
+  if (w == NW - 1) {
     const int d = ldl_warp<R>(o, p.tau * p.tau, true);
     if (lane == 0) o.deg = d;
+    trw(8);
+  } else if (active) {
+    strided_sum<float>(p.Q_part + (size_t)(T.col0 + qs_cols.x) * R, (size_t)p.m * R, p.nr, nqc * R,
+                       reinterpret_cast<float*>(gscr), [&](int e, float v) { qsm[e] = v; }, tid, NCW * 32,
+                       SyncCompute());
+    tr(7);
   }
   __syncthreads();
   if (stamp) p.stats->t_ns[10] = gtimer();
-  const bool deg = o.deg != 0;
-  if (deg) {
-    nb++;
-    orth_slow<R>(p, T, o, ps, ps2, gscr, nb, active);
-  } else if (tid < 32) {
-    o.rep[tid] = 0;
-  }
-  __syncthreads();
   tr(5);
-  // warp 0: kappa estimate (explicit inverse); warps 1..: P_hat rows by forward substitution
-  if (w == 0) inverse_warp<R>(o);
-  else if (active) band_solve<R>(ps, ps2, T.th, o, 32);
-  __syncthreads();
+  // Fused path (reading C20): P_hat = D^-1/2 L^-1 P and Q = D^-1/2 L^-1 Q~ (row
+  // by row) on the compute warps, while warp NW-1 computes Li, kappa and amp.
+  // The fused Q is exact up to rounding; its rounding error is amplified by
+  // amp = ||S Li^T|| (= 1/sigma_min of the column-equilibrated P, ~sqrt(r) for
+  // a warm-started P).  A degenerate column or a forced CholQR2 pass takes the
+  // general path at once; kappa > kappa_thr or amp > amp_thr is checked after
+  // phase 5 when every cell is TMEM-resident (spec; the redo recomputes from
+  // TMEM), else right here.
+  const bool deg = o.deg != 0;
+  bool fused = !deg && !p.force_two_pass;
+  float* phat = ps2;
+  if (fused) {
+    if (w == NW - 1) {
+      inverse_warp<R>(o);
+      trw(15);
+    } else if (active) {
+      solve_rows<R>(ps, H8, T.th, qsm, nqc, o, ps2, p.Qout + (size_t)(T.col0 + qs_cols.x) * R);
+    }
+    if (!p.spec) {
+      __syncthreads();
+      fused = !(o.kappa > p.kappa_thr || o.amp > p.amp_thr);
+    }
+  }
+  if (!fused) {
+    nb = cold_orth_q<R, MBF>(p, T, o, ps, ps2, gscr, pa, taddr_w, nb, active, deg);
+    phat = ps;
+  }
   tr(12);
-  const bool need2 = p.force_two_pass || o.kappa > p.kappa_thr;
-  if (stamp) p.stats->t_ns[11] = gtimer();
-  if (active) {
-    for (int x = tid; x < H8 * RP; x += NT) ps[x] = (x / RP < T.th) ? ps2[x] : 0.f;
+  for (int pass = 0;; pass++) {
+    if (w < NCW) {
+      // ---------------------------------------------------------- tables, B3 (compute warps)
+      SyncCompute()();   // P_hat rows of every compute thread are written
+      if (active) {
+        if (T.cb == 0)
+          for (int x = tid; x < T.th * R; x += NCW * 32)
+            p.Pout[((size_t)T.row0 + x / R) * R + x % R] = phat[(x / R) * RP + x % R];
+        for (int x = tid; x < T.nrblk * KS5 * 32; x += NCW * 32) {  // phase-5 B operand: P_hat^T, N = rows n/2 + 4(n&1)
+          const int ln = x % 32, ks = (x / 32) % KS5, rblk = x / (32 * KS5);
+          const int gg = ln >> 2, tt = ln & 3;
+          const int r = 8 * rblk + (gg >> 1) + 4 * (gg & 1), k = 8 * ks + tt;
+          uint4 v;
+          unsigned h0, l0, h1, l1;
+          split3((k < R) ? phat[r * RP + k] : 0.f, h0, l0);
+          split3((k + 4 < R) ? phat[r * RP + k + 4] : 0.f, h1, l1);
+          v.x = h0; v.y = h1; v.z = l0; v.w = l1;
+          pb[x] = v;
+        }
+      }
+      tr(13);
+      if (stamp) p.stats->t_ns[4] = gtimer();
+      tr(9);
+      nb++;
+      grid_barrier_group(p.bar, nb * gridDim.x, SyncCompute());
+      tr(10);
+      if (stamp) p.stats->t_ns[5] = gtimer();
+
+      // ---------------------------------------------------------- phase 5 (compute warps)
+      if (active) {
+        for (int x = tid; x < T.tw * R; x += NCW * 32) qsm[x] = __ldcg(p.Qout + (size_t)T.col0 * R + x);
+      }
+      SyncCompute()();
+      if (active) {
+        for (int cg = w; cg < T.ncg; cg += NCW) {
+          unsigned qh[KS5][4], ql[KS5][4];
+          {  // A operand Q (M = columns 2g | 2g+1, K = rank)
+            const int cl = 16 * cg + 2 * g;
+            const bool okA = cl < T.tw, okB = cl + 1 < T.tw;
+            const float* qa_ = qsm + (size_t)cl * R;
+#pragma unroll
+            for (int ks = 0; ks < KS5; ks++) {
+              const int k0 = 8 * ks + t;
+              const float a0 = (okA && k0 < R) ? qa_[k0] : 0.f;
+              const float a1 = (okB && k0 < R) ? qa_[R + k0] : 0.f;
+              const float a2 = (okA && k0 + 4 < R) ? qa_[k0 + 4] : 0.f;
+              const float a3 = (okB && k0 + 4 < R) ? qa_[R + k0 + 4] : 0.f;
+              split3(a0, qh[ks][0], ql[ks][0]);
+              split3(a1, qh[ks][1], ql[ks][1]);
+              split3(a2, qh[ks][2], ql[ks][2]);
+              split3(a3, qh[ks][3], ql[ks][3]);
+            }
+          }
+          for (int rb0 = 0; rb0 < T.nrblk; rb0 += 4) {
+            float v16[16];
+            const int cs0 = cell_slot(rb0, cg);
+            const bool batch = cs0 + 4 <= TMEM_CELLS;
+            if (batch) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
+            else cells4_slow<MBF>(p, T, taddr_w, rb0, cg, cs0, g, t, v16);
+            float mr4[4][4];   // four cells, four independent MMA chains
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) mr4[jj][0] = mr4[jj][1] = mr4[jj][2] = mr4[jj][3] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < KS5; ks++)
+#pragma unroll
+              for (int jj = 0; jj < 4; jj++) {
+                const int rblk = min(rb0 + jj, T.nrblk - 1);
+                const uint4 b = pb[(rblk * KS5 + ks) * 32 + lane];
+                mma3(mr4[jj], qh[ks], ql[ks], b.x, b.y, b.z, b.w);
+              }
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) {
+              const int rblk = rb0 + jj;
+              if (rblk >= T.nrblk) break;
+              float* mr = mr4[jj];
+              const float v[4] = {v16[4 * jj], v16[4 * jj + 1], v16[4 * jj + 2], v16[4 * jj + 3]};
+              if (MBF) {
+#pragma unroll
+                for (int q = 0; q < 4; q++) mr[q] = __bfloat162float(__float2bfloat16_rn(mr[q]));
+              }
+              // mr/v: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
+              const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
+              if (r + 4 < T.th && c + 1 < T.tw) {   // both rows and both columns inside: 8-byte pair stores
+                const size_t o0 = (size_t)(T.row0 + r) * p.ldr + (T.col0 + c);
+                if (p.recon) {
+                  if (MBF) {
+                    __nv_bfloat162* d0 = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + o0);
+                    __nv_bfloat162* d1 =
+                        reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + o0 + 4 * p.ldr);
+                    *d0 = __floats2bfloat162_rn(mr[0], mr[2]);
+                    *d1 = __floats2bfloat162_rn(mr[1], mr[3]);
+                  } else {
+                    float* d = reinterpret_cast<float*>(p.recon) + o0;
+                    *reinterpret_cast<float2*>(d) = make_float2(mr[0], mr[2]);
+                    *reinterpret_cast<float2*>(d + 4 * p.ldr) = make_float2(mr[1], mr[3]);
+                  }
+                }
+                if (p.err_out) {
+                  float* d = p.err_out + (size_t)(T.row0 + r) * p.lde_out + (T.col0 + c);
+                  *reinterpret_cast<float2*>(d) = make_float2(v[0] - mr[0], v[2] - mr[2]);
+                  *reinterpret_cast<float2*>(d + 4 * p.lde_out) = make_float2(v[1] - mr[1], v[3] - mr[3]);
+                }
+                continue;
+              }
+              store_cell_edge<MBF>(p, T, r, c, make_float4(mr[0], mr[1], mr[2], mr[3]),
+                                   make_float4(v[0], v[1], v[2], v[3]));
+            }
+          }
+        }
+      }
+      if (stamp) p.stats->t_ns[6] = gtimer();
+      tr(11);
+    }
+    __syncthreads();   // warp NW-1's conditioning estimates are complete
+    // spec check (uniform over the grid: every CTA holds the same G): on failure
+    // redo the general path from TMEM and run tables / B3 / phase 5 again
+    if (pass > 0 || !fused || !(o.kappa > p.kappa_thr || o.amp > p.amp_thr)) break;
+    nb = cold_orth_q<R, MBF>(p, T, o, ps, ps2, gscr, pa, taddr_w, nb, active, false);
+    phat = ps;
+    fused = false;
   }
   if (blockIdx.x == 0 && tid == 0) {
     int cnt = 0;
-    for (int j = 0; j < R; j++) cnt += o.rep[j];
+    if (deg)
+      for (int j = 0; j < R; j++) cnt += o.rep[j];
     p.stats->fallback_columns = cnt;
-    p.stats->second_pass = need2 ? 1 : 0;
+    p.stats->second_pass = (p.force_two_pass || o.kappa > p.kappa_thr) ? 1 : 0;
     p.stats->kappa_est = o.kappa;
+    p.stats->q_amp = deg ? -1.0 : o.amp;
+    p.stats->q_fused = fused ? 1 : 0;
   }
-  __syncthreads();
-  if (need2) {
-    nb++;
-    second_pass<R>(p, T, o, ps, ps2, gscr, nb, active);
-  }
-  if (stamp) p.stats->t_ns[3] = gtimer();
-  tr(13);
-  uint4* pa = reinterpret_cast<uint4*>(sm + p.off_pa);   // [nrblk][MT][32][2] (hi, lo)
-  uint4* pb = reinterpret_cast<uint4*>(sm + p.off_pb);   // [nrblk][KS5][32]   (h0, h1, l0, l1)
-  if (active) {
-    if (T.cb == 0)
-      for (int x = tid; x < T.th * R; x += NT) p.Pout[((size_t)T.row0 + x / R) * R + x % R] = ps[(x / R) * RP + x % R];
-    for (int x = tid; x < T.nrblk * MT * 32; x += NT) {   // phase-3 A operand: P_hat^T, K = rows t, t+4
-      const int ln = x % 32, mt = (x / 32) % MT, rblk = x / (32 * MT);
-      const int gg = ln >> 2, tt = ln & 3;
-      const int r0 = 8 * rblk + tt, k0 = 16 * mt + gg;
-      float v[4];
-      v[0] = (k0 < R) ? ps[r0 * RP + k0] : 0.f;
-      v[1] = (k0 + 8 < R) ? ps[r0 * RP + k0 + 8] : 0.f;
-      v[2] = (k0 < R) ? ps[(r0 + 4) * RP + k0] : 0.f;
-      v[3] = (k0 + 8 < R) ? ps[(r0 + 4) * RP + k0 + 8] : 0.f;
-      uint4 hi, lo;
-      split3(v[0], hi.x, lo.x); split3(v[1], hi.y, lo.y); split3(v[2], hi.z, lo.z); split3(v[3], hi.w, lo.w);
-      pa[2 * x] = hi;
-      pa[2 * x + 1] = lo;
-    }
-    for (int x = tid; x < T.nrblk * KS5 * 32; x += NT) {  // phase-5 B operand: P_hat^T, N = rows n/2 + 4(n&1)
-      const int ln = x % 32, ks = (x / 32) % KS5, rblk = x / (32 * KS5);
-      const int gg = ln >> 2, tt = ln & 3;
-      const int r = 8 * rblk + (gg >> 1) + 4 * (gg & 1), k = 8 * ks + tt;
-      uint4 v;
-      unsigned h0, l0, h1, l1;
-      split3((k < R) ? ps[r * RP + k] : 0.f, h0, l0);
-      split3((k + 4 < R) ? ps[r * RP + k + 4] : 0.f, h1, l1);
-      v.x = h0; v.y = h1; v.z = l0; v.w = l1;
-      pb[x] = v;
-    }
-  }
-  __syncthreads();
-  tr(6);
-  // phase 3a: Q_part[rb][cols] = A_tile^T P_hat_band, complete per column group in one warp
-  if (active) {
-    for (int cg = w; w < NCW && cg < T.ncg; cg += NCW) {
-      float qa2[2][MT][2][4];   // [row-block parity]: two independent accumulator chains
-#pragma unroll
-      for (int pr = 0; pr < 2; pr++)
-#pragma unroll
-        for (int mt = 0; mt < MT; mt++)
-#pragma unroll
-          for (int nt = 0; nt < 2; nt++) qa2[pr][mt][nt][0] = qa2[pr][mt][nt][1] = qa2[pr][mt][nt][2] = qa2[pr][mt][nt][3] = 0.f;
-      for (int rb0 = 0; rb0 < T.nrblk; rb0 += 4) {
-        float v16[16];
-        const int cs0 = cell_slot(rb0, cg);
-        const bool batch = cs0 + 4 <= TMEM_CELLS;
-        if (batch) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
-        else fetch_slow(rb0, cg, cs0, v16);
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
-          const int rblk = rb0 + jj;
-          if (rblk >= T.nrblk) break;
-          const float v[4] = {v16[4 * jj], v16[4 * jj + 1], v16[4 * jj + 2], v16[4 * jj + 3]};
-          unsigned vh[4], vl[4];
-#pragma unroll
-          for (int q = 0; q < 4; q++) split3(v[q], vh[q], vl[q]);
-#pragma unroll
-          for (int mt = 0; mt < MT; mt++) {
-            const uint4 h = pa[2 * ((rblk * MT + mt) * 32 + lane)], l = pa[2 * ((rblk * MT + mt) * 32 + lane) + 1];
-            const unsigned ah[4] = {h.x, h.y, h.z, h.w}, al[4] = {l.x, l.y, l.z, l.w};
-            mma3(qa2[jj & 1][mt][0], ah, al, vh[0], vh[1], vl[0], vl[1]);   // even columns 2g
-            mma3(qa2[jj & 1][mt][1], ah, al, vh[2], vh[3], vl[2], vl[3]);   // odd columns 2g+1
-          }
-        }
-      }
-      float qa[MT][2][4];
-#pragma unroll
-      for (int mt = 0; mt < MT; mt++)
-#pragma unroll
-        for (int nt = 0; nt < 2; nt++)
-#pragma unroll
-          for (int q = 0; q < 4; q++) qa[mt][nt][q] = qa2[0][mt][nt][q] + qa2[1][mt][nt][q];
-      // D[k][n]: c0 = (k=16mt+g, n=2t), c1 = (g, 2t+1), c2 = (g+8, 2t), c3 = (g+8, 2t+1); column = 2n + nt
-      float* dst = p.Q_part + ((size_t)T.rb * p.m + T.col0 + 16 * cg) * R;
-#pragma unroll
-      for (int mt = 0; mt < MT; mt++)
-#pragma unroll
-        for (int nt = 0; nt < 2; nt++) {
-          const int col = 4 * t + nt, k = 16 * mt + g;
-          if (16 * cg + col < T.tw) {
-            if (k < R) dst[col * R + k] = qa[mt][nt][0];
-            if (k + 8 < R) dst[col * R + k + 8] = qa[mt][nt][2];
-          }
-          if (16 * cg + col + 2 < T.tw) {
-            if (k < R) dst[(col + 2) * R + k] = qa[mt][nt][1];
-            if (k + 8 < R) dst[(col + 2) * R + k + 8] = qa[mt][nt][3];
-          }
-        }
-    }
-  }
-  tr(7);
-  gbar();
-  tr(8);
-  if (stamp) p.stats->t_ns[4] = gtimer();
-
-  // ============================================================== phase 4
-  if (active) {
-    const int tot = T.tw * R;
-    const int per = (tot + p.nr - 1) / p.nr;
-    const int x0 = min(tot, T.rb * per), x1 = min(tot, x0 + per);
-    float* qscr = reinterpret_cast<float*>(gscr);
-    strided_sum<float>(p.Q_part + (size_t)T.col0 * R + x0, (size_t)p.m * R, p.nr, x1 - x0, qscr,
-                       [&](int e, float v) { p.Qout[(size_t)T.col0 * R + x0 + e] = v; });
-  }
-  tr(9);
-  gbar();
-  tr(10);
-  if (stamp) p.stats->t_ns[5] = gtimer();
-
-  // ============================================================== phase 5
-  float* qsm = reinterpret_cast<float*>(sm + p.off_qsm);   // [tw][R] Q of this tile's columns
-  if (active) {
-    for (int x = tid; x < T.tw * R; x += NT) qsm[x] = __ldcg(p.Qout + (size_t)T.col0 * R + x);
-  }
-  __syncthreads();
-  if (active) {
-    for (int cg = w; w < NCW && cg < T.ncg; cg += NCW) {
-      unsigned qh[KS5][4], ql[KS5][4];
-      {  // A operand Q (M = columns 2g | 2g+1, K = rank)
-        const int cl = 16 * cg + 2 * g;
-        const bool okA = cl < T.tw, okB = cl + 1 < T.tw;
-        const float* qa_ = qsm + (size_t)cl * R;
-#pragma unroll
-        for (int ks = 0; ks < KS5; ks++) {
-          const int k0 = 8 * ks + t;
-          const float a0 = (okA && k0 < R) ? qa_[k0] : 0.f;
-          const float a1 = (okB && k0 < R) ? qa_[R + k0] : 0.f;
-          const float a2 = (okA && k0 + 4 < R) ? qa_[k0 + 4] : 0.f;
-          const float a3 = (okB && k0 + 4 < R) ? qa_[R + k0 + 4] : 0.f;
-          split3(a0, qh[ks][0], ql[ks][0]);
-          split3(a1, qh[ks][1], ql[ks][1]);
-          split3(a2, qh[ks][2], ql[ks][2]);
-          split3(a3, qh[ks][3], ql[ks][3]);
-        }
-      }
-      for (int rb0 = 0; rb0 < T.nrblk; rb0 += 4) {
-        float v16[16];
-        const int cs0 = cell_slot(rb0, cg);
-        const bool batch = cs0 + 4 <= TMEM_CELLS;
-        if (batch) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
-        else fetch_slow(rb0, cg, cs0, v16);
-        float mr4[4][4];   // four cells, four independent MMA chains
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) mr4[jj][0] = mr4[jj][1] = mr4[jj][2] = mr4[jj][3] = 0.f;
-#pragma unroll
-        for (int ks = 0; ks < KS5; ks++)
-#pragma unroll
-          for (int jj = 0; jj < 4; jj++) {
-            const int rblk = min(rb0 + jj, T.nrblk - 1);
-            const uint4 b = pb[(rblk * KS5 + ks) * 32 + lane];
-            mma3(mr4[jj], qh[ks], ql[ks], b.x, b.y, b.z, b.w);
-          }
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
-          const int rblk = rb0 + jj;
-          if (rblk >= T.nrblk) break;
-          float* mr = mr4[jj];
-          const float v[4] = {v16[4 * jj], v16[4 * jj + 1], v16[4 * jj + 2], v16[4 * jj + 3]};
-          if (MBF) {
-#pragma unroll
-            for (int q = 0; q < 4; q++) mr[q] = __bfloat162float(__float2bfloat16_rn(mr[q]));
-          }
-          // mr/v: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
-          const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
-          if (r + 4 < T.th && c + 1 < T.tw) {   // both rows and both columns inside: 8-byte pair stores
-            const size_t o0 = (size_t)(T.row0 + r) * p.ldr + (T.col0 + c);
-            if (p.recon) {
-              if (MBF) {
-                __nv_bfloat162* d0 = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + o0);
-                __nv_bfloat162* d1 = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + o0 + 4 * p.ldr);
-                *d0 = __floats2bfloat162_rn(mr[0], mr[2]);
-                *d1 = __floats2bfloat162_rn(mr[1], mr[3]);
-              } else {
-                float* d = reinterpret_cast<float*>(p.recon) + o0;
-                *reinterpret_cast<float2*>(d) = make_float2(mr[0], mr[2]);
-                *reinterpret_cast<float2*>(d + 4 * p.ldr) = make_float2(mr[1], mr[3]);
-              }
-            }
-            if (p.err_out) {
-              float* d = p.err_out + (size_t)(T.row0 + r) * p.lde_out + (T.col0 + c);
-              *reinterpret_cast<float2*>(d) = make_float2(v[0] - mr[0], v[2] - mr[2]);
-              *reinterpret_cast<float2*>(d + 4 * p.lde_out) = make_float2(v[1] - mr[1], v[3] - mr[3]);
-            }
-            continue;
-          }
-          store_cell_edge<MBF>(p, T, r, c, make_float4(mr[0], mr[1], mr[2], mr[3]), make_float4(v[0], v[1], v[2], v[3]));
-        }
-      }
-    }
-  }
-  if (stamp) p.stats->t_ns[6] = gtimer();
-  tr(11);
 
   // ============================================================== teardown
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

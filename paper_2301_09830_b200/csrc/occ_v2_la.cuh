@@ -1,0 +1,358 @@
+// occ_v2_la.cuh -- small fp64 linear algebra of the fused step (reading C3-C5,
+// C20): the Gram partials and their reduction, the warp-level LDL^T, the
+// explicit D^-1/2 L^-1 with the conditioning estimates, the slow-path LDL with
+// column substitution, and the row solves.  Included by occ_v2.cu and by the
+// single-warp micro-benchmark tools/la_bench.cu.
+#pragma once
+#include "occ_v2.cuh"
+
+namespace occ {
+namespace v2 {
+
+template <int R>
+struct K {
+  static constexpr int RP = R < 8 ? 8 : R;   // padded rank
+  static constexpr int MT = (RP + 15) / 16;  // m-tiles of 16 over the rank
+  static constexpr int KS5 = RP / 8;         // phase-5 k-steps
+  static constexpr int NP = npairs(R);
+};
+
+constexpr int LD = 33;   // padded stride of the small fp64 matrices: conflict-free rows and columns
+
+struct OrthW {  // small fp64 linear algebra in shared memory
+  double L[32 * LD];    // Gram (full), then the unit lower factor of G = L D L^T
+  double Li[32 * LD];   // D^-1/2 L^-1: P_hat = P Li^T
+  double X[32 * LD];    // P^T F (slow path)
+  double Y[32 * LD];    // F^T F (slow path)
+  double gdiag[32];     // diag(G): each column's own squared norm (degeneracy test)
+  double D[32];
+  double col[32];       // per-step broadcast buffer
+  double dinv[32];      // D^-1/2
+  int rep[32];
+  int deg;
+  double kappa;
+  double amp;           // ||S Li^T||_F, S = diag(||p_j||): error amplification of Q = (A^T P) Li^T
+};
+
+struct SyncAll {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct SyncCompute {   // the NCW compute warps 0 .. NCW-1 (named barrier 1)
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory"); }
+};
+
+// out[e] = sum_{u < S} src[u * stride + e], e < E, in a fixed order (deterministic),
+// by the threads x in [0, nthr) of a group synchronised by sync().  Every thread
+// keeps 16 independent loads in flight: the partial sums live in L2 and this is
+// latency bound.  scratch: nthr elements of shared memory.
+template <typename Tv, typename Fout, typename Sync = SyncAll>
+__device__ void strided_sum(const Tv* __restrict__ src, size_t stride, int S, int E, Tv* scratch, Fout&& out,
+                            int x = threadIdx.x, int nthr = NT, Sync sync = Sync()) {
+  for (int e0 = 0; e0 < E; e0 += nthr) {
+    const int En = min(nthr, E - e0);
+    const int C = max(1, nthr / En);
+    Tv acc = Tv(0);
+    if (x < En * C) {
+      const int e = e0 + x % En, c = x / En;
+      for (int u0 = c; u0 < S; u0 += 16 * C) {
+        Tv v[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const int u = u0 + j * C;
+          v[j] = (u < S) ? __ldcg(src + (size_t)u * stride + e) : Tv(0);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j++) acc += v[j];
+      }
+    }
+    sync();
+    if (x < En * C) scratch[x] = acc;
+    sync();
+    if (x < En) {
+      Tv r = Tv(0);
+      for (int c = 0; c < C; c++) r += scratch[c * En + x];
+      out(e0 + x, r);
+    }
+    sync();
+  }
+}
+
+// G (packed upper triangle, nparts partials) -> o.L (full symmetric), o.gdiag.  All threads.
+template <int R>
+__device__ void reduce_partials(const double* __restrict__ part, int nparts, OrthW& o, double* scratch) {
+  constexpr int NP = K<R>::NP;
+  strided_sum<double>(part, NP, nparts, NP, scratch, [&](int q, double gsum) {
+    int a = 0, rem = q;
+    while (rem >= R - a) { rem -= R - a; a++; }
+    const int b = a + rem;
+    o.L[a * LD + b] = gsum;
+    o.L[b * LD + a] = gsum;
+    if (a == b) o.gdiag[a] = gsum;
+  });
+}
+
+// 1/d for normal d > 0: MUFU reciprocal estimate + two Newton steps (full fp64
+// accuracy; roughly half the latency of the IEEE division on the LDL chain).
+__device__ __forceinline__ double rcp_fast(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Warp-level right-looking LDL^T of the Gram in o.L (R <= 32), square-root free
+// so the sequential chain per column is one fp64 reciprocal.  Lane i holds row
+// i in registers; column j is broadcast through o.col.  detect: stop at the
+// first column whose squared residual D_j is below tau2 * its own squared norm
+// (reading C3: the MGS test ||v|| < tau ||p_j||) and return 1 (o.L is then
+// left as it was).  One warp.  Fully unrolled: one warp runs this alone, so the
+// dynamic instruction count is its latency (a rolled variant with predicated
+// register selects measured 2.3x slower, tools/la_bench.cu).
+template <int R>
+__device__ int ldl_warp(OrthW& o, double tau2, bool detect) {
+  const int i = threadIdx.x & 31;
+  double row[R];
+#pragma unroll
+  for (int k = 0; k < R; k++) row[k] = (i < R) ? o.L[i * LD + k] : 0.0;
+  int deg = 0;
+#pragma unroll
+  for (int j = 0; j < R; j++) {
+    if (i >= j && i < R) o.col[i] = row[j];   // u_i = G_ij after the previous updates
+    __syncwarp();
+    const double d = o.col[j];
+    const double gj = o.gdiag[j];
+    if (detect && (gj == 0.0 || !(d >= tau2 * gj))) { deg = 1; break; }
+    const double rinv = rcp_fast(d > 0.0 ? d : 1e-300);
+    const double lij = row[j] * rinv;
+#pragma unroll
+    for (int k = j + 1; k < R; k++)
+      if (i >= k && i < R) row[k] = fma(-lij, o.col[k], row[k]);
+    if (i > j) row[j] = lij;
+    if (i == j) { o.D[j] = d; row[j] = 1.0; }
+    __syncwarp();
+  }
+  if (!deg && i < R) {
+#pragma unroll
+    for (int k = 0; k < R; k++) o.L[i * LD + k] = (k <= i) ? row[k] : 0.0;
+    o.dinv[i] = 1.0 / sqrt(o.D[i]);
+  }
+  __syncwarp();
+  return deg;
+}
+
+// o.Li = D^-1/2 L^-1 for the unit lower L; kappa = ||L D^1/2||_F ||D^-1/2 L^-1||_F
+// (>= cond_2(P)), amp = ||S Li^T||_F with S = diag(sqrt(G_jj)).  One warp;
+// lane c owns column c of L^-1 (fully unrolled, see ldl_warp).
+template <int R>
+__device__ void inverse_warp(OrthW& o) {
+  const int c = threadIdx.x & 31;
+  double col[R];
+#pragma unroll
+  for (int i = 0; i < R; i++) {
+    double v0 = (i == c) ? 1.0 : 0.0, v1 = 0.0;   // two chains for ILP
+#pragma unroll
+    for (int k = 0; k < i; k++) {
+      if (k & 1) v1 = fma(-o.L[i * LD + k], col[k], v1);
+      else v0 = fma(-o.L[i * LD + k], col[k], v0);
+    }
+    col[i] = (i >= c && c < R) ? v0 + v1 : 0.0;
+  }
+  const double sdc = (c < R) ? sqrt(o.D[c] > 0.0 ? o.D[c] : 0.0) : 0.0;
+  double nl = 0.0, ni = 0.0;
+  if (c < R) {
+#pragma unroll
+    for (int i = 0; i < R; i++) {
+      const double v = col[i] * o.dinv[i];
+      o.Li[i * LD + c] = v;
+      ni = fma(v, v, ni);
+      const double lc = o.L[i * LD + c] * sdc;   // (L D^1/2)[i][c]
+      nl = fma(lc, lc, nl);
+    }
+  }
+  double na = (c < R) ? o.gdiag[c] * ni : 0.0;   // ||p_c||^2 * ||Li[:, c]||^2
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    nl += __shfl_xor_sync(0xffffffffu, nl, off);
+    ni += __shfl_xor_sync(0xffffffffu, ni, off);
+    na += __shfl_xor_sync(0xffffffffu, na, off);
+  }
+  if (c == 0) {
+    o.kappa = sqrt(nl) * sqrt(ni);
+    o.amp = sqrt(na);
+  }
+  __syncwarp();
+}
+
+// The hot-path factorisation: LDL^T with the degenerate-column test, then (if
+// no column is degenerate) Li, kappa and amp.  One out-of-line instance, so a
+// dry run on an identity matrix (kernel phase 2) warms exactly this code.
+template <int R>
+__device__ __noinline__ int la_factor(OrthW& o, double tau2) {
+  const int d = ldl_warp<R>(o, tau2, true);
+  if (!d) inverse_warp<R>(o);
+  return d;
+}
+
+// Up-looking LDL^T with column substitution (slow path, thread 0): the Gram of
+// the modified column set c_j = rep[j] ? f_j : p_j is read from o.L (P^T P),
+// o.X (P^T F) and o.Y (F^T F); a column failing the test is replaced once.
+template <int R>
+__device__ __noinline__ void ldl_subst(OrthW& o, double tau2) {
+  if (threadIdx.x != 0) return;
+  double* Lt = o.Li;  // scratch; o.L keeps P^T P until the end
+  for (int x = 0; x < 32 * LD; x++) Lt[x] = 0.0;
+  for (int j = 0; j < R; j++) o.rep[j] = 0;
+  auto gram = [&](int a, int b) -> double {
+    const bool ra = o.rep[a], rb = o.rep[b];
+    if (!ra && !rb) return o.L[a * LD + b];
+    if (!ra && rb) return o.X[a * LD + b];
+    if (ra && !rb) return o.X[b * LD + a];
+    return o.Y[a * LD + b];
+  };
+  for (int i = 0; i < R; i++) {
+    for (int attempt = 0; attempt < 2; attempt++) {
+      for (int k = 0; k < i; k++) {
+        double v = gram(i, k);
+        for (int l = 0; l < k; l++) v -= Lt[i * LD + l] * o.D[l] * Lt[k * LD + l];
+        Lt[i * LD + k] = v / o.D[k];
+      }
+      const double g = gram(i, i);
+      double d = g;
+      for (int k = 0; k < i; k++) d -= Lt[i * LD + k] * Lt[i * LD + k] * o.D[k];
+      if (attempt == 0 && (g == 0.0 || !(d >= tau2 * g))) { o.rep[i] = 1; continue; }
+      o.D[i] = d > 0.0 ? d : 1e-300;
+      Lt[i * LD + i] = 1.0;
+      break;
+    }
+  }
+  for (int x = 0; x < 32 * LD; x++) o.L[x] = Lt[x];
+  for (int j = 0; j < R; j++) o.dinv[j] = 1.0 / sqrt(o.D[j]);
+}
+
+// P_hat rows = D^-1/2 L^-1 P[i] by forward substitution with the unit lower
+// L of G = L D L^T (no explicit inverse on the critical path).  One thread
+// per row, threads [t0, t0 + nthr).
+// On the slow path ps already holds P_m (substituted columns replaced by their
+// fallback vectors, orth_slow).  fp64, rounded to fp32.
+template <int R>
+__device__ void band_solve(const float* ps, float* out, int nr, const OrthW& o, int t0, int nthr) {
+  constexpr int RP = K<R>::RP;
+  for (int i = (int)threadIdx.x - t0; i < nr && i >= 0 && (int)threadIdx.x < t0 + nthr; i += nthr) {
+    double x[R];
+#pragma unroll
+    for (int a = 0; a < R; a++) {
+      double v0 = (double)ps[i * RP + a];
+      double v1 = 0.0;
+#pragma unroll
+      for (int b = 0; b < a; b++) {
+        if (b & 1) v1 = fma(-o.L[a * LD + b], x[b], v1);
+        else v0 = fma(-o.L[a * LD + b], x[b], v0);
+      }
+      x[a] = v0 + v1;
+    }
+#pragma unroll
+    for (int a = 0; a < R; a++) out[i * RP + a] = (float)(x[a] * o.dinv[a]);
+  }
+}
+
+// Fused path (reading C20): rows x -> D^-1/2 L^-1 x by forward substitution
+// with the unit lower L of G = L D L^T, for the H8 rows of the P band (rows >= th
+// zero; -> P_hat) and the nqc rows of the reduced Q~ slice (-> Q).  One row per
+// thread of the NCW compute warps; fp64, rounded to fp32.
+template <int R>
+__device__ __forceinline__ void solve_rows(const float* ps, int H8, int th, const float* qt, int nqc, const OrthW& o,
+                                           float* phat, float* qout) {
+  constexpr int RP = K<R>::RP;
+  for (int it = threadIdx.x; it < H8 + nqc; it += NCW * 32) {
+    const bool isP = it < H8;
+    const float* src = isP ? ps + (size_t)it * RP : qt + (size_t)(it - H8) * R;
+    const bool zero = isP && it >= th;
+    double x[R];
+#pragma unroll
+    for (int a = 0; a < R; a++) {
+      double v0 = zero ? 0.0 : (double)src[a], v1 = 0.0;
+#pragma unroll
+      for (int b = 0; b < a; b++) {
+        if (b & 1) v1 = fma(-o.L[a * LD + b], x[b], v1);
+        else v0 = fma(-o.L[a * LD + b], x[b], v0);
+      }
+      x[a] = v0 + v1;
+    }
+    float* dst = isP ? phat + (size_t)it * RP : qout + (size_t)(it - H8) * R;
+#pragma unroll
+    for (int a = 0; a < R; a++) dst[a] = (float)(x[a] * o.dinv[a]);
+  }
+}
+
+// Gram partial (packed) of rows [0,nr) of an fp32 [.][RP] array, fp64.
+template <int R>
+__device__ void band_gram(const float* ps, int nr, double* part, double* scratch) {
+  constexpr int RP = K<R>::RP, NP = K<R>::NP;
+  const int gsz = max(1, (int)blockDim.x / NP);
+  for (int x = threadIdx.x; x < NP * gsz; x += blockDim.x) {
+    const int q = x % NP, grp = x / NP;
+    int a = 0, rem = q;
+    while (rem >= R - a) { rem -= R - a; a++; }
+    const int b = a + rem;
+    double gg = 0.0;
+    for (int i = grp; i < nr; i += gsz) gg = fma((double)ps[i * RP + a], (double)ps[i * RP + b], gg);
+    scratch[x] = gg;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < NP; q += blockDim.x) {
+    double gg = 0.0;
+    for (int grp = 0; grp < gsz; grp++) gg += scratch[grp * NP + q];
+    part[q] = gg;
+  }
+}
+
+// fp64 tensor-core MMA, D(8x8) += A(8x4) B(4x8); lane l holds A[l/4][l%4],
+// B[l%4][l/4], D[l/4][2(l%4)], D[l/4][2(l%4)+1].
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Gram partial (packed upper triangle) of rows [0,nr) of an fp32 [.][RP] array
+// (RP = 8 MT8; rows >= nr of the array are zero up to a multiple of 4), fp64 on
+// the tensor cores (DMMA), by ONE warp while the other warps compute Q_part.
+// G = P^T P: A = P^T, B = P; tile (mi, nj) of 8x8, mi <= nj; two accumulator
+// sets (even / odd k-steps).  Fixed order: deterministic.
+template <int R>
+__device__ void band_gram_warp(const float* ps, int nr, double* part) {
+  constexpr int RP = K<R>::RP, T8 = RP / 8, NT8 = T8 * (T8 + 1) / 2;
+  const int lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+  double acc[2][NT8][2];
+#pragma unroll
+  for (int h = 0; h < 2; h++)
+#pragma unroll
+    for (int u = 0; u < NT8; u++) acc[h][u][0] = acc[h][u][1] = 0.0;
+  const int nk = (nr + 3) / 4;
+  for (int ks = 0; ks < nk; ks++) {
+    const int row = 4 * ks + tq;   // K index of this lane
+    double v[T8];                   // P[row][8 t + gq]: A-fragment of tile t, and B-fragment of tile t
+#pragma unroll
+    for (int t8 = 0; t8 < T8; t8++) v[t8] = (row < nr) ? (double)ps[row * RP + 8 * t8 + gq] : 0.0;
+    int u = 0;
+#pragma unroll
+    for (int mi = 0; mi < T8; mi++)
+#pragma unroll
+      for (int nj = mi; nj < T8; nj++, u++) dmma(acc[ks & 1][u], v[mi], v[nj]);
+  }
+  int u = 0;
+#pragma unroll
+  for (int mi = 0; mi < T8; mi++)
+#pragma unroll
+    for (int nj = mi; nj < T8; nj++, u++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int a = 8 * mi + gq, b = 8 * nj + 2 * tq + h;
+        if (a <= b && b < R) part[a * R - a * (a - 1) / 2 + (b - a)] = acc[0][u][h] + acc[1][u][h];
+      }
+}
+
+}  // namespace v2
+}  // namespace occ

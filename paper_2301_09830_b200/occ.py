@@ -35,7 +35,7 @@ class occ_mat(ctypes.Structure):
 class occ_stats(ctypes.Structure):
     _fields_ = [("fallback_columns", ctypes.c_int32), ("second_pass", ctypes.c_int32),
                 ("kappa_est", ctypes.c_double), ("path", ctypes.c_int32), ("grid", ctypes.c_int32),
-                ("t_ns", ctypes.c_uint64 * 12)]
+                ("t_ns", ctypes.c_uint64 * 12), ("q_amp", ctypes.c_double), ("q_fused", ctypes.c_int32)]
 
 
 class OccError(RuntimeError):
@@ -198,7 +198,8 @@ def occ_read_stats(ws, stream=None) -> dict:
     st = occ_stats()
     _check(lib().occ_read_stats(ws.data_ptr(), ctypes.byref(st), _stream(stream)), "occ_read_stats")
     return {"fallback_columns": st.fallback_columns, "second_pass": st.second_pass,
-            "kappa_est": st.kappa_est, "path": st.path, "grid": st.grid, "t_ns": list(st.t_ns)}
+            "kappa_est": st.kappa_est, "path": st.path, "grid": st.grid, "t_ns": list(st.t_ns),
+            "q_amp": st.q_amp, "q_fused": st.q_fused}
 
 
 def occ_check_status(stream=None, comm: Optional["Comm"] = None):

@@ -5,9 +5,10 @@ import numpy as np, torch
 from paper_2301_09830_b200 import occ
 from workloads import synth
 
-SEG = [("phase1", 0, 1), ("B1 wait", 1, 2), ("phase2", 2, 3), ("B2 wait", 3, 4), ("reduceG+LDL+inv", 4, 5),
-       ("inv|solve", 5, 12), ("copy+need2", 12, 13), ("tables", 13, 6), ("phase3a", 6, 7), ("B3 wait", 7, 8), ("phase4", 8, 9), ("B4 wait", 9, 10),
-       ("phase5", 10, 11)]
+SEG = [("phase1", 0, 1), ("B1 wait", 1, 2), ("ph2 w0: Pband + Q~part", 2, 3), ("ph2 w15: Pband + gram", 2, 14),
+       ("B2 (w0 arrive -> release)", 3, 4), ("G reduce", 4, 6), ("w15 LDL", 6, 8), ("w0 Q~ reduce", 6, 7),
+       ("sync after LDL", 7, 5), ("w15 inverse (off path)", 5, 15), ("w0 solve (or general path)", 5, 12),
+       ("tables", 12, 13), ("B3 wait", 9, 10), ("phase5", 10, 11)]
 
 
 def run(n, m, r, reps=8):
@@ -44,7 +45,7 @@ def run(n, m, r, reps=8):
         res.setdefault("start skew", []).append(((gt[:, 0].max() - t0) / 1e3,) * 2)
     out = {k: {"median_us": round(float(np.median([x[0] for x in v])), 2), "max_us": round(float(np.median([x[1] for x in v])), 2)}
            for k, v in res.items()}
-    print(json.dumps({"shape": [n, m, r], "grid": g, "second_pass": st["second_pass"], "kappa": st["kappa_est"], "fallback": st["fallback_columns"]}))
+    print(json.dumps({"shape": [n, m, r], "grid": g, "second_pass": st["second_pass"], "kappa": st["kappa_est"], "fallback": st["fallback_columns"], "q_amp": st["q_amp"], "q_fused": st["q_fused"]}))
     for k, v in out.items():
         print(f"  {k:28s} median {v['median_us']:7.2f} us   max {v['max_us']:7.2f} us")
 
