@@ -168,9 +168,9 @@ occ_status occ_check_status(cudaStream_t stream, occ_comm comm);
 /* Copies the diagnostics of the last call that used `ws` (synchronises). */
 occ_status occ_read_stats(const void* ws, occ_stats* out, cudaStream_t stream);
 
-/* Debug: per-CTA phase trace of the last fused (v2) call on ws: out[cta*32 + k],
- * k < 16 clock64 at phase boundaries, k >= 16 the matching %globaltimer (ns).
- * Copies min(count, 160*32) words (synchronises). */
+/* Debug: per-CTA phase trace of the last fused (v2) call on ws: out[cta*48 + k],
+ * k < 24 clock64 at phase boundaries, k >= 24 the matching %globaltimer (ns).
+ * Copies min(count, 160*48) words (synchronises). */
 occ_status occ_read_trace(const void* ws, uint64_t* out, int count, cudaStream_t stream);
 
 #if defined(__GNUC__)

@@ -17,7 +17,7 @@ struct Geometry {
 };
 
 constexpr size_t kTraceOffset = 256;
-constexpr int kTraceSlots = 32;                           // per CTA: 16 clock64 + 16 globaltimer stamps
+constexpr int kTraceSlots = 48;                           // per CTA: 24 clock64 stamps, then the matching globaltimer stamps (v2::kTrStamps)
 constexpr size_t kTraceBytes = 160 * kTraceSlots * 8;     // up to 160 CTAs
 
 struct WsLayout {

@@ -4,6 +4,8 @@
 #include "occ_v2_la.cuh"
 #include "occ_internal.h"
 
+static_assert(2 * occ::v2::kTrStamps == occ::kTraceSlots, "trace layout");
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>

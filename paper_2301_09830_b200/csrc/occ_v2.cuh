@@ -47,6 +47,7 @@ constexpr int NCW = NW - 1;     // compute warps; warp NW-1 is the phase-1 copy 
 constexpr int SR = 8;           // tile rows per staging stage (one cell row block)
 constexpr int MAX_STAGES = 4;
 constexpr int TMEM_CELLS = 512 / (NW / 4) / 4;  // cells per warp in TMEM (its columns / 4)
+constexpr int kTrStamps = 24;   // per-CTA phase-trace stamps (occ_read_trace)
 
 struct Params2 {
   const void* M; long long ldm;
@@ -68,7 +69,7 @@ struct Params2 {
   double* XY_band;     // [nr][2 R R]
   float* Q_part;       // [nr][m][R]
   unsigned* bar;
-  unsigned long long* trace;   // [grid][32]: clock64 stamps 0..15, globaltimer stamps 16..31
+  unsigned long long* trace;   // [grid][2 kTrStamps]: clock64 stamps, then globaltimer stamps
   DevStats* stats;
   unsigned long long fb_seed;
   double tau, kappa_thr;

@@ -29,14 +29,14 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (stamp) p.stats->t_ns[0] = gtimer();
   auto tr = [&](int k) {   // per-CTA phase trace (occ_read_trace)
     if (tid == 0) {
-      p.trace[blockIdx.x * 32 + k] = clock64();
-      p.trace[blockIdx.x * 32 + 16 + k] = gtimer();
+      p.trace[blockIdx.x * (2 * kTrStamps) + k] = clock64();
+      p.trace[blockIdx.x * (2 * kTrStamps) + kTrStamps + k] = gtimer();
     }
   };
   auto trw = [&](int k) {   // stamp from lane 0 of the calling warp
     if (lane == 0) {
-      p.trace[blockIdx.x * 32 + k] = clock64();
-      p.trace[blockIdx.x * 32 + 16 + k] = gtimer();
+      p.trace[blockIdx.x * (2 * kTrStamps) + k] = clock64();
+      p.trace[blockIdx.x * (2 * kTrStamps) + kTrStamps + k] = gtimer();
     }
   };
   tr(0);
@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   uint4* pa = reinterpret_cast<uint4*>(sm + p.off_pa);   // [nrblk][MT][32][2] (hi, lo)
   uint4* pb = reinterpret_cast<uint4*>(sm + p.off_pb);   // [nrblk][KS5][32]   (h0, h1, l0, l1)
   float* qsm = reinterpret_cast<float*>(sm + p.off_qsm);   // phase 3: Q~ slice; phase 5: [tw][R] Q of the tile
+  if (tid == 0) o.prog = 0;   // ldl_warp publish protocol (phase 3; every CTA, active or not)
   if (active) {
     for (int x = tid; x < H8 * RP; x += NT) {
       const int i = x / RP, k = x % RP;
@@ -292,49 +293,54 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (stamp) p.stats->t_ns[2] = gtimer();
 
   // ============================================================== phase 3
-  // G = sum of the nr band partials (all threads); then warp NW-1 factors it
-  // (LDL^T with the degenerate-column test) while the compute warps reduce
-  // this CTA's column slice of Q~ over the nr row bands.
-  reduce_partials<R>(p.G_band, p.nr, o, gscr);
-  tr(6);
-  if (stamp) p.stats->t_ns[9] = gtimer();
-  const int2 qs_cols = active ? q_slice(T, p.nr) : make_int2(0, 0);
-  const int nqc = qs_cols.y - qs_cols.x;
-  if (w == NW - 1) {
-    const int d = ldl_warp<R>(o, p.tau * p.tau, true);
-    if (lane == 0) o.deg = d;
-    trw(8);
-  } else if (active) {
-    strided_sum<float>(p.Q_part + (size_t)(T.col0 + qs_cols.x) * R, (size_t)p.m * R, p.nr, nqc * R,
-                       reinterpret_cast<float*>(gscr), [&](int e, float v) { qsm[e] = v; }, tid, NCW * 32,
-                       SyncCompute());
-    tr(7);
-  }
-  __syncthreads();
-  if (stamp) p.stats->t_ns[10] = gtimer();
-  tr(5);
-  // Fused path (reading C20): P_hat = D^-1/2 L^-1 P and Q = D^-1/2 L^-1 Q~ (row
-  // by row) on the compute warps, while warp NW-1 computes Li, kappa and amp.
+  // G = sum of the nr band partials (all threads).  Then, concurrently:
+  //   warp NW-1:     LDL^T of G with the degenerate-column test, publishing each
+  //                  column of L as it is final; then Li, kappa, amp (off the
+  //                  critical path: checked after phase 5)
+  //   compute warps: reduce this CTA's column slice of Q~ over the nr row bands,
+  //                  then P_hat = D^-1/2 L^-1 P and Q = D^-1/2 L^-1 Q~ row by row,
+  //                  one step behind the factorisation (reading C20)
   // The fused Q is exact up to rounding; its rounding error is amplified by
   // amp = ||S Li^T|| (= 1/sigma_min of the column-equilibrated P, ~sqrt(r) for
   // a warm-started P).  A degenerate column or a forced CholQR2 pass takes the
   // general path at once; kappa > kappa_thr or amp > amp_thr is checked after
   // phase 5 when every cell is TMEM-resident (spec; the redo recomputes from
-  // TMEM), else right here.
-  const bool deg = o.deg != 0;
-  bool fused = !deg && !p.force_two_pass;
-  float* phat = ps2;
-  if (fused) {
-    if (w == NW - 1) {
+  // TMEM), else before it.
+  reduce_partials<R>(p.G_band, p.nr, o, gscr);
+  tr(6);
+  if (stamp) p.stats->t_ns[9] = gtimer();
+  const int2 qs_cols = active ? q_slice(T, p.nr) : make_int2(0, 0);
+  const int nqc = qs_cols.y - qs_cols.x;
+  const bool force2 = p.force_two_pass != 0;
+  bool deg;
+  if (w == NW - 1) {
+    deg = ldl_warp<R>(o, p.tau * p.tau, true, true) != 0;
+    trw(8);
+    if (!deg && !force2) {
       inverse_warp<R>(o);
       trw(15);
-    } else if (active) {
-      solve_rows<R>(ps, H8, T.th, qsm, nqc, o, ps2, p.Qout + (size_t)(T.col0 + qs_cols.x) * R);
     }
-    if (!p.spec) {
-      __syncthreads();
-      fused = !(o.kappa > p.kappa_thr || o.amp > p.amp_thr);
+  } else {
+    if (active) {
+      strided_sum<float>(p.Q_part + (size_t)(T.col0 + qs_cols.x) * R, (size_t)p.m * R, p.nr, nqc * R,
+                         reinterpret_cast<float*>(gscr), [&](int e, float v) { qsm[e] = v; }, tid, NCW * 32,
+                         SyncCompute());
+      tr(7);
     }
+    if (!force2 && active)
+      deg = !solve_rows_pipelined<R>(ps, H8, T.th, qsm, nqc, o, ps2, p.Qout + (size_t)(T.col0 + qs_cols.x) * R);
+    else
+      deg = !wait_prog(o, R + 1);
+  }
+  if (stamp) p.stats->t_ns[10] = gtimer();
+  tr(5);
+  bool fused = !deg && !force2;   // uniform over the grid (every CTA factors the same G)
+  float* phat = ps2;
+  if (fused && !p.spec) {
+    __syncthreads();
+    fused = !(o.kappa > p.kappa_thr || o.amp > p.amp_thr);
+  } else if (!fused) {
+    __syncthreads();
   }
   if (!fused) {
     nb = cold_orth_q<R, MBF>(p, T, o, ps, ps2, gscr, pa, taddr_w, nb, active, deg);
@@ -403,14 +409,16 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
             float mr4[4][4];   // four cells, four independent MMA chains
 #pragma unroll
             for (int jj = 0; jj < 4; jj++) mr4[jj][0] = mr4[jj][1] = mr4[jj][2] = mr4[jj][3] = 0.f;
+            if (!(p.debug & 64)) {   // (debug 64: no phase-5 MMAs, timing experiment)
 #pragma unroll
-            for (int ks = 0; ks < KS5; ks++)
+              for (int ks = 0; ks < KS5; ks++)
 #pragma unroll
-              for (int jj = 0; jj < 4; jj++) {
-                const int rblk = min(rb0 + jj, T.nrblk - 1);
-                const uint4 b = pb[(rblk * KS5 + ks) * 32 + lane];
-                mma3(mr4[jj], qh[ks], ql[ks], b.x, b.y, b.z, b.w);
-              }
+                for (int jj = 0; jj < 4; jj++) {
+                  const int rblk = min(rb0 + jj, T.nrblk - 1);
+                  const uint4 b = pb[(rblk * KS5 + ks) * 32 + lane];
+                  mma3(mr4[jj], qh[ks], ql[ks], b.x, b.y, b.z, b.w);
+                }
+            }
 #pragma unroll
             for (int jj = 0; jj < 4; jj++) {
               const int rblk = rb0 + jj;
@@ -423,6 +431,10 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
               }
               // mr/v: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
               const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
+              if (p.debug & 32) {   // timing experiment: no phase-5 stores
+                if (mr[0] == 1.2345f && v[0] == 5.4321f) p.stats->grid = -1;
+                continue;
+              }
               if (r + 4 < T.th && c + 1 < T.tw) {   // both rows and both columns inside: 8-byte pair stores
                 const size_t o0 = (size_t)(T.row0 + r) * p.ldr + (T.col0 + c);
                 if (p.recon) {

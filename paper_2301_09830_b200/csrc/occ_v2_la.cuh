@@ -30,6 +30,7 @@ struct OrthW {  // small fp64 linear algebra in shared memory
   double dinv[32];      // D^-1/2
   int rep[32];
   int deg;
+  int prog;             // ldl_warp progress (publish mode): steps done; R + 1 = finished; -1 = degenerate
   double kappa;
   double amp;           // ||S Li^T||_F, S = diag(||p_j||): error amplification of Q = (A^T P) Li^T
 };
@@ -103,75 +104,93 @@ __device__ __forceinline__ double rcp_fast(double d) {
 }
 
 // Warp-level right-looking LDL^T of the Gram in o.L (R <= 32), square-root free
-// so the sequential chain per column is one fp64 reciprocal.  Lane i holds row
-// i in registers; column j is broadcast through o.col.  detect: stop at the
-// first column whose squared residual D_j is below tau2 * its own squared norm
-// (reading C3: the MGS test ||v|| < tau ||p_j||) and return 1 (o.L is then
-// left as it was).  One warp.  Fully unrolled: one warp runs this alone, so the
-// dynamic instruction count is its latency (a rolled variant with predicated
-// register selects measured 2.3x slower, tools/la_bench.cu).
+// so the sequential chain per column is one fp64 reciprocal.  Lane i holds the
+// active part of row i in registers, SHIFTED: at step j, rr[k] = a_{i, j+k}; the
+// update writes rr[k-1] = rr[k] - l_ij a_{j+k, j}, so the pivot is always rr[0]
+// and every register index is static while the step loop stays rolled (this
+// code runs once per call, usually from a cold instruction cache: its size is
+// part of its latency; tools/la_bench.cu).  Column j (unscaled) is broadcast
+// through o.col; L (unit lower) is stored into o.L column by column.  detect:
+// stop at the first column whose squared residual D_j is below tau2 * its own
+// squared norm (reading C3: the MGS test ||v|| < tau ||p_j||) and return 1 (o.L
+// is then partially overwritten; callers re-reduce it).  publish: advance o.prog
+// after every column, so solve_rows_pipelined can trail one step behind.
 template <int R>
-__device__ int ldl_warp(OrthW& o, double tau2, bool detect) {
+__device__ int ldl_warp(OrthW& o, double tau2, bool detect, bool publish = false) {
   const int i = threadIdx.x & 31;
-  double row[R];
+  double rr[R];
 #pragma unroll
-  for (int k = 0; k < R; k++) row[k] = (i < R) ? o.L[i * LD + k] : 0.0;
+  for (int k = 0; k < R; k++) rr[k] = (i < R) ? o.L[i * LD + k] : 0.0;
   int deg = 0;
-#pragma unroll
+#pragma unroll 1
   for (int j = 0; j < R; j++) {
-    if (i >= j && i < R) o.col[i] = row[j];   // u_i = G_ij after the previous updates
+    if (i >= j && i < R) o.col[i] = rr[0];   // a_ij of the current Schur complement
     __syncwarp();
     const double d = o.col[j];
     const double gj = o.gdiag[j];
-    if (detect && (gj == 0.0 || !(d >= tau2 * gj))) { deg = 1; break; }
-    const double rinv = rcp_fast(d > 0.0 ? d : 1e-300);
-    const double lij = row[j] * rinv;
+    double cv[R - 1];
 #pragma unroll
-    for (int k = j + 1; k < R; k++)
-      if (i >= k && i < R) row[k] = fma(-lij, o.col[k], row[k]);
-    if (i > j) row[j] = lij;
-    if (i == j) { o.D[j] = d; row[j] = 1.0; }
+    for (int k = 1; k < R; k++) cv[k - 1] = o.col[min(j + k, R - 1)];   // a_{j+k, j} (k > R-1-j: unused)
+    if (detect && (gj == 0.0 || !(d >= tau2 * gj))) { deg = 1; break; }
+    const double lij = (i > j && i < R) ? rr[0] * rcp_fast(d > 0.0 ? d : 1e-300) : 0.0;
+#pragma unroll
+    for (int k = 1; k < R; k++) rr[k - 1] = fma(-lij, cv[k - 1], rr[k]);
+    rr[R - 1] = 0.0;
+    if (i > j && i < R) o.L[i * LD + j] = lij;
+    if (i == j) o.D[j] = d;
     __syncwarp();
+    if (publish && i == 0) {
+      __threadfence_block();
+      *reinterpret_cast<volatile int*>(&o.prog) = j + 1;
+    }
   }
   if (!deg && i < R) {
-#pragma unroll
-    for (int k = 0; k < R; k++) o.L[i * LD + k] = (k <= i) ? row[k] : 0.0;
+#pragma unroll 1
+    for (int k = i; k < R; k++) o.L[i * LD + k] = (k == i) ? 1.0 : 0.0;
     o.dinv[i] = 1.0 / sqrt(o.D[i]);
   }
   __syncwarp();
+  if (publish && i == 0) {
+    __threadfence_block();
+    *reinterpret_cast<volatile int*>(&o.prog) = deg ? -1 : R + 1;
+  }
   return deg;
 }
 
 // o.Li = D^-1/2 L^-1 for the unit lower L; kappa = ||L D^1/2||_F ||D^-1/2 L^-1||_F
 // (>= cond_2(P)), amp = ||S Li^T||_F with S = diag(sqrt(G_jj)).  One warp;
-// lane c owns column c of L^-1 (fully unrolled, see ldl_warp).
+// lane c forms column c of L^-1 by forward substitution in place in o.Li
+// (conflict-free: lanes touch consecutive words of a row).  Compact rolled
+// loops: on the fused path this runs off the critical path.
 template <int R>
 __device__ void inverse_warp(OrthW& o) {
   const int c = threadIdx.x & 31;
-  double col[R];
-#pragma unroll
-  for (int i = 0; i < R; i++) {
-    double v0 = (i == c) ? 1.0 : 0.0, v1 = 0.0;   // two chains for ILP
-#pragma unroll
-    for (int k = 0; k < i; k++) {
-      if (k & 1) v1 = fma(-o.L[i * LD + k], col[k], v1);
-      else v0 = fma(-o.L[i * LD + k], col[k], v0);
-    }
-    col[i] = (i >= c && c < R) ? v0 + v1 : 0.0;
-  }
-  const double sdc = (c < R) ? sqrt(o.D[c] > 0.0 ? o.D[c] : 0.0) : 0.0;
-  double nl = 0.0, ni = 0.0;
+  double* X = o.Li;
   if (c < R) {
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < R; i++) {
-      const double v = col[i] * o.dinv[i];
-      o.Li[i * LD + c] = v;
+      double v0 = (i == c) ? 1.0 : 0.0, v1 = 0.0;
+#pragma unroll 2
+      for (int k = c; k < i; k++) {
+        if (k & 1) v1 = fma(-o.L[i * LD + k], X[k * LD + c], v1);
+        else v0 = fma(-o.L[i * LD + k], X[k * LD + c], v0);
+      }
+      X[i * LD + c] = (i >= c) ? v0 + v1 : 0.0;
+    }
+  }
+  double nl = 0.0, ni = 0.0, na = 0.0;
+  if (c < R) {
+    const double sdc = sqrt(o.D[c] > 0.0 ? o.D[c] : 0.0);
+#pragma unroll 1
+    for (int i = 0; i < R; i++) {
+      const double v = X[i * LD + c] * o.dinv[i];
+      X[i * LD + c] = v;
       ni = fma(v, v, ni);
       const double lc = o.L[i * LD + c] * sdc;   // (L D^1/2)[i][c]
       nl = fma(lc, lc, nl);
     }
+    na = o.gdiag[c] * ni;   // ||p_c||^2 * ||Li[:, c]||^2
   }
-  double na = (c < R) ? o.gdiag[c] * ni : 0.0;   // ||p_c||^2 * ||Li[:, c]||^2
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
     nl += __shfl_xor_sync(0xffffffffu, nl, off);
@@ -185,14 +204,13 @@ __device__ void inverse_warp(OrthW& o) {
   __syncwarp();
 }
 
-// The hot-path factorisation: LDL^T with the degenerate-column test, then (if
-// no column is degenerate) Li, kappa and amp.  One out-of-line instance, so a
-// dry run on an identity matrix (kernel phase 2) warms exactly this code.
-template <int R>
-__device__ __noinline__ int la_factor(OrthW& o, double tau2) {
-  const int d = ldl_warp<R>(o, tau2, true);
-  if (!d) inverse_warp<R>(o);
-  return d;
+// Wait until ldl_warp (publish mode) has passed step `a` (o.prog >= a); returns
+// false if it stopped at a degenerate column.
+__device__ __forceinline__ bool wait_prog(const OrthW& o, int a) {
+  int pv;
+  while ((pv = *reinterpret_cast<const volatile int*>(&o.prog)) < a && pv >= 0) __nanosleep(32);
+  __threadfence_block();
+  return pv >= 0;
 }
 
 // Up-looking LDL^T with column substitution (slow path, thread 0): the Gram of
@@ -255,6 +273,52 @@ __device__ void band_solve(const float* ps, float* out, int nr, const OrthW& o, 
 #pragma unroll
     for (int a = 0; a < R; a++) out[i * RP + a] = (float)(x[a] * o.dinv[a]);
   }
+}
+
+// Fused path (reading C20), pipelined behind ldl_warp(publish): every row x of
+// the P band (rows >= th zero; -> P_hat) and of the reduced Q~ slice (-> Q)
+// becomes D^-1/2 L^-1 x by right-looking substitution: at step a, x_a is final
+// once column a of L is (o.prog > a), and x_{a+k} -= l_{a+k,a} x_a.  The
+// registers are shifted like ldl_warp's: xr[k] holds x_{a+k}; the finished x_a
+// enters at xr[R-1] and shifts left with the rest (its l is 0), so after R steps
+// xr[k] = x_k.  Rows are spread over the compute warps that do not share warp
+// NW-1's scheduler (w % 4 != 3), so the spinning leaves the factorisation's
+// issue slots alone.  Returns false (writes nothing) if the factorisation
+// stopped at a degenerate column.
+template <int R>
+__device__ __forceinline__ bool solve_rows_pipelined(const float* ps, int H8, int th, const float* qt, int nqc,
+                                                     const OrthW& o, float* phat, float* qout) {
+  constexpr int RP = K<R>::RP;
+  const int w = threadIdx.x >> 5;
+  bool ok = true;
+  if ((w & 3) != 3) {
+    const int slot = (w - (w >> 2)) * 32 + (threadIdx.x & 31);   // dense index over the solver warps
+    constexpr int NSOLVE = (NCW - NCW / 4) * 32;
+    for (int it = slot; it < H8 + nqc; it += NSOLVE) {
+      const bool isP = it < H8;
+      const float* src = isP ? ps + (size_t)it * RP : qt + (size_t)(it - H8) * R;
+      const bool zero = isP && it >= th;
+      double xr[R];
+#pragma unroll
+      for (int k = 0; k < R; k++) xr[k] = zero ? 0.0 : (double)src[k];
+#pragma unroll 1
+      for (int a = 0; a < R; a++) {
+        if (!wait_prog(o, a + 1)) { ok = false; break; }
+        const double xa = xr[0];
+        double lv[R - 1];
+#pragma unroll
+        for (int k = 1; k < R; k++) lv[k - 1] = (a + k < R) ? o.L[(a + k) * LD + a] : 0.0;
+#pragma unroll
+        for (int k = 1; k < R; k++) xr[k - 1] = fma(-lv[k - 1], xa, xr[k]);
+        xr[R - 1] = xa;
+      }
+      if (!ok || !wait_prog(o, R + 1)) { ok = false; break; }
+      float* dst = isP ? phat + (size_t)it * RP : qout + (size_t)(it - H8) * R;
+#pragma unroll
+      for (int k = 0; k < R; k++) dst[k] = (float)(xr[k] * o.dinv[k]);
+    }
+  }
+  return ok && wait_prog(o, R + 1);
 }
 
 // Fused path (reading C20): rows x -> D^-1/2 L^-1 x by forward substitution

@@ -133,6 +133,40 @@ def test_paths_deterministic_and_consistent(monkeypatch):
     assert rel(a["err"], b1["err"], A) <= 1e-5
 
 
+@pytest.mark.parametrize("debug,fused", [(0, 1), (4, 0), (16, 1), (20, 0)])
+def test_v2_control_flows(monkeypatch, debug, fused):
+    """The fused kernel's phase-3 control flows (reading C20), all against the
+    oracle: fused Q checked after phase 5 (0), the same with the post-phase-5
+    redo forced (4: amp gate -1), the check before phase 5 (16), and the
+    general path taken before phase 5 (20)."""
+    n, m, r = 1000, 1208, 16
+    M = synth.d2_gradlike(n, m, 61)
+    e = synth.e0(n, m, 62, like=M)
+    Q0 = synth.q0(m, r, 63)
+    monkeypatch.setenv("OCC_V2_DEBUG", str(debug))
+    g = run_gpu(M, e, Q0, r)
+    assert g["stats"]["path"] == 3
+    assert g["stats"]["q_fused"] == fused
+    assert 0 < g["stats"]["q_amp"] < 32
+    o = oracle.compress_step(M, e, Q0)
+    check_step(g, o, M.astype(np.float64) + e, tol=TOL32)
+
+
+def test_amp_gate_rejects_collinear_factor():
+    """Nearly collinear Q_prev columns make P nearly collinear: the fused
+    Q = (A^T P) Li^T would amplify rounding by amp >> 32, so the kernel must
+    recompute Q = A^T P_hat (q_fused = 0) and still match the oracle."""
+    n, m, r = 1000, 1208, 16
+    M = synth.d2_gradlike(n, m, 71)
+    e = synth.e0(n, m, 72, like=M)
+    base = synth.q0(m, 1, 73)
+    Q0 = (base + 1e-3 * synth.q0(m, r, 74)).astype(np.float32)
+    g = run_gpu(M, e, Q0, r)
+    assert g["stats"]["q_fused"] == 0 and g["stats"]["q_amp"] > 32
+    o = oracle.compress_step(M, e, Q0)
+    check_step(g, o, M.astype(np.float64) + e, tol=TOL32, check_factors=False)
+
+
 def test_zero_input_all_fallbacks():
     n, m, r = 300, 264, 8
     M = np.zeros((n, m), np.float32)

@@ -5,9 +5,10 @@ import numpy as np, torch
 from paper_2301_09830_b200 import occ
 from workloads import synth
 
+S = 24   # stamps per CTA (kTrStamps)
 SEG = [("phase1", 0, 1), ("B1 wait", 1, 2), ("ph2 w0: Pband + Q~part", 2, 3), ("ph2 w15: Pband + gram", 2, 14),
        ("B2 (w0 arrive -> release)", 3, 4), ("G reduce", 4, 6), ("w15 LDL", 6, 8), ("w0 Q~ reduce", 6, 7),
-       ("sync after LDL", 7, 5), ("w15 inverse (off path)", 5, 15), ("w0 solve (or general path)", 5, 12),
+       ("w0 solve done (after Q~)", 7, 5), ("w15 inverse (off path)", 8, 15), ("general path (if any)", 5, 12),
        ("tables", 12, 13), ("B3 wait", 9, 10), ("phase5", 10, 11)]
 
 
@@ -20,21 +21,21 @@ def run(n, m, r, reps=8):
     ws = occ.alloc_workspace(n, m, r)
     flush = torch.ones(64 * 1024 * 1024, device="cuda")
     sink = torch.empty(1, device="cuda")
-    buf = (ctypes.c_uint64 * (160 * 32))()
+    buf = (ctypes.c_uint64 * (160 * 2 * S))()
     res = {}
     for i in range(reps):
         if not os.environ.get("NOFLUSH"):
             torch.sum(flush, dim=0, out=sink[0])
         occ.occ_compress(M, E, Q, P, R, r=r, ws=ws)
         torch.cuda.synchronize()
-        assert occ.lib().occ_read_trace(ws.data_ptr(), buf, 160 * 32, None) == 0
+        assert occ.lib().occ_read_trace(ws.data_ptr(), buf, 160 * 2 * S, None) == 0
         st = occ.occ_read_stats(ws)
         if i < 3:
             continue
         g = st["grid"]
-        tr = np.array(buf[: g * 32], dtype=np.float64).reshape(g, 32)
-        gt = tr[:, 16:]
-        ck = tr[:, :16]
+        tr = np.array(buf[: g * 2 * S], dtype=np.float64).reshape(g, 2 * S)
+        gt = tr[:, S:]
+        ck = tr[:, :S]
         t0 = gt[:, 0].min()
         for name, a, b in SEG:
             d = (gt[:, b] - gt[:, a]) / 1e3
