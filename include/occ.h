@@ -94,7 +94,7 @@ typedef struct {
   double kappa_est;         /* ||L||_F * ||L^-1||_F of the first Cholesky factor (>= cond_2(P)) */
   int32_t path;             /* 1 = fused persistent kernel (v1), 2 = one launch per phase, 3 = TMEM-resident fused kernel (v2) */
   int32_t grid;             /* CTAs of the persistent kernel */
-  uint64_t t_ns[12];        /* %globaltimer stamps of CTA 0 at phase boundaries (diagnostic) */
+  uint64_t t_ns[12];        /* %globaltimer stamps of CTA 0 at phase boundaries (diagnostic; the v2 kernel fills them only in the OCC_TRACE build) */
   double q_amp;             /* v2: ||S Li^T||_F, the rounding amplification of the fused Q = (A^T P) Li^T; -1 if not computed */
   int32_t q_fused;          /* v2: 1 if Q was formed as (A^T P) Li^T (reading C20), 0 if as A^T P_hat */
 } occ_stats;
@@ -168,7 +168,8 @@ occ_status occ_check_status(cudaStream_t stream, occ_comm comm);
 /* Copies the diagnostics of the last call that used `ws` (synchronises). */
 occ_status occ_read_stats(const void* ws, occ_stats* out, cudaStream_t stream);
 
-/* Debug: per-CTA phase trace of the last fused (v2) call on ws: out[cta*48 + k],
+/* Debug (libocc_trace.so, built with -DOCC_TRACE; the product library leaves
+ * the trace zero): per-CTA phase trace of the last fused (v2) call on ws: out[cta*48 + k],
  * k < 24 clock64 at phase boundaries, k >= 24 the matching %globaltimer (ns).
  * Copies min(count, 160*48) words (synchronises). */
 occ_status occ_read_trace(const void* ws, uint64_t* out, int count, cudaStream_t stream);

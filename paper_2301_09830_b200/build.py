@@ -1,6 +1,10 @@
 """Builds libocc.so (the C-ABI library of include/occ.h) in-tree for sm_100a.
 
-    python -m paper_2301_09830_b200.build [--force]
+    python -m paper_2301_09830_b200.build [--force] [--trace]
+
+--trace also builds libocc_trace.so: the same library compiled with
+-DOCC_TRACE (per-CTA phase stamps for tools/trace.py).  The product library
+carries no instrumentation.
 
 nvcc cross-compiles without a GPU.  The NCCL it links is the one bundled with
 torch (nvidia/nccl), found through an rpath so that the process shares a
@@ -16,6 +20,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libocc.so")
+LIB_TRACE = os.path.join(HERE, "libocc_trace.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("occ_api.cu", "occ_step.cu", "occ_v2.cu")]
 DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + \
     glob.glob(os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "occ.h")]
@@ -42,19 +47,21 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    lib = LIB_TRACE if trace else LIB
+    if not force and up_to_date(lib):
+        return lib
     nd = nccl_dir()
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc(), *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
+           *(["-DOCC_TRACE"] if trace else []),
            "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nd, "include"),
            *SOURCES, "-L" + os.path.join(nd, "lib"), "-l:libnccl.so.2",
            "-Xlinker", "-rpath," + os.path.join(nd, "lib"), "-o", tmp]
@@ -62,9 +69,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--trace" in sys.argv:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace=True))

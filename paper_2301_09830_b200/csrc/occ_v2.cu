@@ -7,6 +7,8 @@
 static_assert(2 * occ::v2::kTrStamps == occ::kTraceSlots, "trace layout");
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -240,7 +242,37 @@ static double row_eff(int bytes) {
 }
 
 template <int R>
+static Plan2 plan_search(int64_t n, int64_t m, int sms, bool mbf);
+
+// Plans are looked up on every call (occ_workspace_bytes, occ_compress): a
+// small cache keeps the host cost of a call independent of the search.
+template <int R>
 static Plan2 plan_for(int64_t n, int64_t m, int sms, bool mbf) {
+  struct Entry {
+    int64_t n = -1, m = -1;
+    int sms = 0;
+    bool mbf = false;
+    Plan2 plan;
+  };
+  constexpr int kEntries = 16;
+  static Entry cache[kEntries];
+  static int next = 0;
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry& e : cache)
+      if (e.n == n && e.m == m && e.sms == sms && e.mbf == mbf) return e.plan;
+  }
+  const Plan2 pl = plan_search<R>(n, m, sms, mbf);
+  std::lock_guard<std::mutex> lk(mu);
+  Entry& e = cache[next];
+  next = (next + 1) % kEntries;
+  e.n = n; e.m = m; e.sms = sms; e.mbf = mbf; e.plan = pl;
+  return pl;
+}
+
+template <int R>
+static Plan2 plan_search(int64_t n, int64_t m, int sms, bool mbf) {
   constexpr int RP = K<R>::RP, MT = K<R>::MT, KS5 = K<R>::KS5, NP = K<R>::NP;
   Plan2 best;
   const int smem_cap = 227 * 1024 - 2048;
@@ -339,8 +371,20 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
   p.amp_thr = (p.debug & 4) ? -1.0 : 32.0;
   p.spec = (pl.cells_per_warp <= TMEM_CELLS && !(p.debug & 16)) ? 1 : 0;
   auto kern = occ_v2_kernel<R, MBF>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
+  // the dynamic-SMEM opt-in only ever grows; set it when a plan needs more
+  // (per device: the attribute is per-context state)
+  static std::atomic<int> smem_set[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
+  std::atomic<int>& cur = smem_set[dev & 63];
+  if (pl.total > cur.load(std::memory_order_relaxed)) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.total);
+    if (e != cudaSuccess) return e;
+    int seen = cur.load();
+    while (pl.total > seen && !cur.compare_exchange_weak(seen, pl.total)) {
+    }
+  }
   void* args[] = {&p};
   return cudaLaunchCooperativeKernel((const void*)kern, dim3(pl.nr * pl.nc), dim3(NT), args, pl.total, st);
 }

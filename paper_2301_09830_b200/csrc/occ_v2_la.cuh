@@ -44,8 +44,9 @@ struct SyncCompute {   // the NCW compute warps 0 .. NCW-1 (named barrier 1)
 
 // out[e] = sum_{u < S} src[u * stride + e], e < E, in a fixed order (deterministic),
 // by the threads x in [0, nthr) of a group synchronised by sync().  Every thread
-// keeps 16 independent loads in flight: the partial sums live in L2 and this is
-// latency bound.  scratch: nthr elements of shared memory.
+// keeps 8 independent loads in flight (the partial sums live in L2 and this is
+// latency bound; 8 rather than 16 halves the code, which runs once per call
+// from a cold instruction cache).  scratch: nthr elements of shared memory.
 template <typename Tv, typename Fout, typename Sync = SyncAll>
 __device__ void strided_sum(const Tv* __restrict__ src, size_t stride, int S, int E, Tv* scratch, Fout&& out,
                             int x = threadIdx.x, int nthr = NT, Sync sync = Sync()) {
@@ -55,15 +56,15 @@ __device__ void strided_sum(const Tv* __restrict__ src, size_t stride, int S, in
     Tv acc = Tv(0);
     if (x < En * C) {
       const int e = e0 + x % En, c = x / En;
-      for (int u0 = c; u0 < S; u0 += 16 * C) {
-        Tv v[16];
+      for (int u0 = c; u0 < S; u0 += 8 * C) {
+        Tv v[8];
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
+        for (int j = 0; j < 8; j++) {
           const int u = u0 + j * C;
           v[j] = (u < S) ? __ldcg(src + (size_t)u * stride + e) : Tv(0);
         }
 #pragma unroll
-        for (int j = 0; j < 16; j++) acc += v[j];
+        for (int j = 0; j < 8; j++) acc += v[j];
       }
     }
     sync();

@@ -12,7 +12,8 @@ import os
 from typing import Optional, Sequence
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libocc.so")
+# OCC_LIB=trace selects the instrumented build (libocc_trace.so, tools/trace.py)
+LIB_PATH = os.path.join(HERE, "libocc_trace.so" if os.environ.get("OCC_LIB") == "trace" else "libocc.so")
 
 OCC_F32, OCC_BF16 = 0, 1
 OCC_NO_EF = 1
