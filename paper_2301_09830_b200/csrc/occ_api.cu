@@ -94,8 +94,9 @@ occ_status check_step(const occ_mat& M, const occ_mat& err, const occ_mat& Q, co
   if (need_err || err.ptr) {
     if ((s = check_view(err, "err", M.rows, M.cols, true, false))) return s;
   }
-  if ((s = check_view(Q, "Q", M.cols, r, true, true))) return s;
-  if ((s = check_view(P, "P", M.rows, r, true, true))) return s;
+  const bool ot = (flags & OCC_ORIENT_T) != 0;   // P on the column side, Q on the row side
+  if ((s = check_view(Q, "Q", ot ? M.rows : M.cols, r, true, true))) return s;
+  if ((s = check_view(P, "P", ot ? M.cols : M.rows, r, true, true))) return s;
   if (recon && recon->ptr) {
     if ((s = check_view(*recon, "recon", M.rows, M.cols, false, false))) return s;
     if (recon->dtype != M.dtype) return fail(OCC_ERR_DTYPE, "recon: dtype must equal M's");
@@ -158,6 +159,23 @@ occ_status nccl_fail(ncclResult_t r, const char* what) {
   return fail(OCC_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
 }
 
+// Phase ranges of run_phases (occ_step.cu PhaseId): [0,2) = sweep 1 + P reduce,
+// [2,6) = Gram + orthonormalisation, [6,8) = sweep 2 + Q reduce, [8,9) = reconstruct.
+constexpr int kPhA = 0, kPhOrth = 2, kPhD = 6, kPhF = 8, kPhEnd = 9;
+
+// Orthonormalise the column-side factor U (m x R, in place) with the per-phase
+// kernels: the Gram phases run with the factor length m (OCC_ORIENT_T).
+cudaError_t orth_column_factor(const Params& base, float* U, int64_t m, int64_t n, int R, const WsLayout& L,
+                               void* ws, bool multi, cudaStream_t st) {
+  Params p2 = base;
+  p2.n = (int)m;
+  p2.m = (int)n;
+  p2.P = U;
+  Geometry gT = make_geometry(m, n, R, kGeomSms);
+  fill_ws(p2, gT, L, ws);
+  return run_phases(p2, gT, kPhOrth, kPhD, multi, false, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -213,6 +231,31 @@ occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat re
   p.ldr = recon.ptr ? recon.ld : 0;
   fill_ws(p, g, L, ws);
   const bool multi = want_multi(flags);
+  if (flags & OCC_ORIENT_T) {
+    // the step on A^T in A's layout (reading C6): U = A^T Q_prev (sweep 2 with the
+    // row-side warm start), U_hat = orth(U) into P, V = A U_hat (sweep 1) into Q
+    // (the next warm start), M' = V U_hat^T, e_new = A - M'
+    float* Pp = static_cast<float*>(P.ptr);
+    float* Qp = static_cast<float*>(Q.ptr);
+    Params p1 = p;
+    p1.P = Qp;
+    p1.Qloc = Pp;
+    cudaError_t e = run_phases(p1, g, kPhD, kPhF, multi, false, stream);
+    if (e == cudaSuccess) e = orth_column_factor(p, Pp, M.cols, M.rows, r, L, ws, multi, stream);
+    if (e == cudaSuccess) {
+      Params p3 = p;
+      p3.Qprev = Pp;
+      p3.P = Qp;
+      e = run_phases(p3, g, kPhA, kPhOrth, multi, false, stream);
+    }
+    if (e == cudaSuccess) {
+      Params p4 = p;
+      p4.P = Qp;
+      p4.Qrec = Pp;
+      e = run_phases(p4, g, kPhF, kPhEnd, multi, false, stream);
+    }
+    return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_compress (OCC_ORIENT_T) launch");
+  }
   if (!multi && !want_v1() && L.v2_tail_bytes > 0) {
     cudaError_t e2 = run_v2(p, r, static_cast<char*>(ws) + L.v2_tail, L.v2_tail_bytes, kGeomSms, stream);
     if (e2 == cudaSuccess) return OCC_OK;
@@ -287,6 +330,55 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
     fill_ws(p, g, L, ws);
     return std::make_pair(p, g);
   };
+  if (flags & OCC_ORIENT_T) {
+    // DP step on A_w^T (reading C6), in A's layout: U_w = A_w^T V_prev (column
+    // side) -> allreduce-sum U -> U_hat = orth(U) into P -> V_w = A_w U_hat (row
+    // side) -> allreduce-sum V -> M' = (scale V_sum) U_hat^T, e_w = A_w - V_w U_hat^T
+    // (local, reading C2) or A_w - M'; Q <- scale V_sum (the warm start).
+    for (int i = 0; i < nmat; i++) {
+      auto [p, g] = params_for(i);
+      p.P = static_cast<float*>(Q[i].ptr);
+      p.Qloc = qwb + qoff[i];
+      cudaError_t e = run_phases(p, g, kPhD, kPhF, multi, false, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "dp (ORIENT_T) sweep launch");
+    }
+    if (comm) {
+      ncclResult_t nr = ncclAllReduce(qwb, qwb, qtot, ncclFloat, ncclSum, dp->comm, stream);
+      if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(U)");
+    }
+    for (int i = 0; i < nmat; i++) {
+      auto [p, g] = params_for(i);
+      float* Up = static_cast<float*>(P[i].ptr);
+      cudaError_t e = cudaMemcpyAsync(Up, qwb + qoff[i], (size_t)G[i].cols * R * 4, cudaMemcpyDeviceToDevice, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "U copy");
+      e = orth_column_factor(p, Up, G[i].cols, G[i].rows, R, L, ws, multi, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "dp (ORIENT_T) orthonormalise launch");
+      p.Qprev = Up;
+      p.P = pb + poff[i];
+      e = run_phases(p, g, kPhA, kPhOrth, multi, false, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "dp (ORIENT_T) sweep launch");
+    }
+    float* vsum = pb;
+    if (comm) {
+      ncclResult_t nr = ncclAllReduce(pb, qsb, ptot, ncclFloat, ncclSum, dp->comm, stream);
+      if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(V)");
+      vsum = qsb;
+    }
+    for (int i = 0; i < nmat; i++) {
+      auto [p, g] = params_for(i);
+      p.P = vsum + poff[i];
+      p.Qrec = static_cast<const float*>(P[i].ptr);
+      p.Ploc = dpl ? pb + poff[i] : nullptr;
+      p.Pstate_out = static_cast<float*>(Q[i].ptr);
+      p.scale = scale;
+      p.dp_local_err = dpl ? 1 : 0;
+      p.recon = G[i].ptr;
+      p.ldr = G[i].ld;
+      cudaError_t e = run_phases(p, g, kPhF, kPhEnd, multi, dpl, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "dp (ORIENT_T) reconstruct launch");
+    }
+    return OCC_OK;
+  }
   // (a1-a2) sweep 1 + P reduce for every matrix into the P bucket
   for (int i = 0; i < nmat; i++) {
     auto [p, g] = params_for(i);
@@ -340,27 +432,27 @@ occ_status occ_send_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r,
   if (s) return s;
   ncclResult_t nr;
   if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
-  ncclSend(P.ptr, (size_t)M.rows * r, ncclFloat, peer, pp->comm, stream);
-  ncclSend(Q.ptr, (size_t)M.cols * r, ncclFloat, peer, pp->comm, stream);
+  ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream);   // (OCC_ORIENT_T: P is m x r)
+  ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream);
   if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclSend(P,Q)");
   return OCC_OK;
 }
 
 occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, uint32_t flags, occ_comm pp,
                             cudaStream_t stream) {
-  (void)flags;
   if (!pp) return fail(OCC_ERR_INVALID_ARG, "pp communicator is null");
   if (peer < 0 || peer >= pp->nranks || peer == pp->rank) return fail(OCC_ERR_INVALID_ARG, "bad peer %d", peer);
   if ((int)P.cols != r) return fail(OCC_ERR_SHAPE, "P: cols must equal r");
-  occ_status s = check_view(P, "P", out.rows, r, true, true);
+  const bool ot = (flags & OCC_ORIENT_T) != 0;   // P m x r, Q n x r; out = Q P^T
+  occ_status s = check_view(P, "P", ot ? out.cols : out.rows, r, true, true);
   if (s) return s;
-  if ((s = check_view(Q, "Q", out.cols, r, true, true))) return s;
+  if ((s = check_view(Q, "Q", ot ? out.rows : out.cols, r, true, true))) return s;
   ncclResult_t nr;
   if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
-  ncclRecv(P.ptr, (size_t)out.rows * r, ncclFloat, peer, pp->comm, stream);
-  ncclRecv(Q.ptr, (size_t)out.cols * r, ncclFloat, peer, pp->comm, stream);
+  ncclRecv(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream);
+  ncclRecv(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream);
   if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclRecv(P,Q)");
-  return occ_decompress(P, Q, out, stream);
+  return ot ? occ_decompress(Q, P, out, stream) : occ_decompress(P, Q, out, stream);
 }
 
 occ_status occ_embed_sync(occ_mat G, occ_mat err, occ_mat Q, occ_mat P, int r, float scale, uint32_t flags,

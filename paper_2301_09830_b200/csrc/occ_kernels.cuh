@@ -61,6 +61,10 @@ struct Params {
   float* Qloc;           // m x R: written by E (local Q_w)
   const float* Qrec;     // m x R: Q used for M' in F (1 GPU: == Qloc; DP: allreduced sum)
   float* Qstate_out;     // m x R: if set, F writes scale * Qrec (DP warm start)
+  // OCC_ORIENT_T, DP (reading C6): the orthonormal factor is on the column side
+  // (Qrec), the exchanged one on the row side (P = the reduced sum)
+  const float* Ploc;     // n x R: if set (DP local convention), e = A - Ploc Qrec^T
+  float* Pstate_out;     // n x R: if set, F writes scale * P (row-side warm start)
   float scale;
   int dp_local_err;      // F: e = A - P_hat Qloc^T (DP local convention, reading C2)
   // workspace
@@ -637,7 +641,9 @@ __device__ void phase_E(const Params& p) {
 }
 
 // ------------------------------------------------------------------ phase F
-// M' = round(P_hat (scale*Qrec)^T);  e_new = A - M'  (or A - P_hat Qloc^T, DP local)
+// M' = round(P_hat (scale*Qrec)^T);  e_new = A - M'  (or A - P_hat Qloc^T, DP local).
+// OCC_ORIENT_T, DP local: e_new = A - Ploc Qrec^T (the local row factor), and
+// the row-side warm start scale * P goes to Pstate_out.
 template <int R, bool DPL>
 __device__ void phase_F(const Params& p, float* sm) {
   constexpr int CPT = CfgF<R, DPL>::CPT, CB = CfgF<R, DPL>::CB;
@@ -645,15 +651,23 @@ __device__ void phase_F(const Params& p, float* sm) {
   const int ncb = (p.m + CB - 1) / CB;
   const int nrb = (p.n + F_ROWS - 1) / F_ROWS;
   const int units = ncb * nrb;
-  float* phs = sm;  // [F_ROWS][R]
+  float* phs = sm;                         // [F_ROWS][R]
+  float* phl = sm + (size_t)F_ROWS * R;    // [F_ROWS][R] Ploc rows (DP, OCC_ORIENT_T)
+  const bool rowloc = DPL && p.Ploc != nullptr;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int rb = u % nrb, cb = u / nrb;
     const int r0 = rb * F_ROWS, nr = min(F_ROWS, p.n - r0);
     const int c = cb * CB + lane * CPT;
     const bool cok = c < p.m;
     __syncthreads();
-    for (int x = threadIdx.x; x < nr * R / 4; x += NT)
-      reinterpret_cast<float4*>(phs)[x] = __ldcg(reinterpret_cast<const float4*>(p.P + (size_t)r0 * R) + x);
+    for (int x = threadIdx.x; x < nr * R / 4; x += NT) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(p.P + (size_t)r0 * R) + x);
+      reinterpret_cast<float4*>(phs)[x] = v;
+      if (p.Pstate_out && cb == 0)
+        reinterpret_cast<float4*>(p.Pstate_out + (size_t)r0 * R)[x] =
+            make_float4(p.scale * v.x, p.scale * v.y, p.scale * v.z, p.scale * v.w);
+      if (rowloc) reinterpret_cast<float4*>(phl)[x] = __ldcg(reinterpret_cast<const float4*>(p.Ploc + (size_t)r0 * R) + x);
+    }
     __syncthreads();
     if (!cok) continue;
     float qv[CPT * R];
@@ -667,8 +681,8 @@ __device__ void phase_F(const Params& p, float* sm) {
         qv[q * R + 4 * k4 + 0] = p.scale * v.x; qv[q * R + 4 * k4 + 1] = p.scale * v.y;
         qv[q * R + 4 * k4 + 2] = p.scale * v.z; qv[q * R + 4 * k4 + 3] = p.scale * v.w;
       }
-      if constexpr (DPL) {
-        const float4* sl = reinterpret_cast<const float4*>(p.Qloc + (size_t)(c + q) * R);
+      if constexpr (DPL) {   // the local column factor (or, with Ploc, Qrec unscaled)
+        const float4* sl = reinterpret_cast<const float4*>((rowloc ? p.Qrec : p.Qloc) + (size_t)(c + q) * R);
 #pragma unroll
         for (int k4 = 0; k4 < R / 4; k4++) {
           float4 v = __ldcg(sl + k4);
@@ -691,12 +705,14 @@ __device__ void phase_F(const Params& p, float* sm) {
       const bool need_a = p.err_out != nullptr;
       if (need_a) load_A<CPT>(p, i, c, a);
       const float4* ph = reinterpret_cast<const float4*>(phs + ii * R);
+      const float4* pl = reinterpret_cast<const float4*>((rowloc ? phl : phs) + ii * R);
       float mr[CPT], ml[CPT];
 #pragma unroll
       for (int q = 0; q < CPT; q++) { mr[q] = 0.f; ml[q] = 0.f; }
 #pragma unroll
       for (int k4 = 0; k4 < R / 4; k4++) {
         const float4 v = ph[k4];
+        const float4 vl = pl[k4];
 #pragma unroll
         for (int q = 0; q < CPT; q++) {
           mr[q] = fmaf(v.x, qv[q * R + 4 * k4 + 0], mr[q]);
@@ -704,10 +720,10 @@ __device__ void phase_F(const Params& p, float* sm) {
           mr[q] = fmaf(v.z, qv[q * R + 4 * k4 + 2], mr[q]);
           mr[q] = fmaf(v.w, qv[q * R + 4 * k4 + 3], mr[q]);
           if constexpr (DPL) {
-            ml[q] = fmaf(v.x, ql[q * R + 4 * k4 + 0], ml[q]);
-            ml[q] = fmaf(v.y, ql[q * R + 4 * k4 + 1], ml[q]);
-            ml[q] = fmaf(v.z, ql[q * R + 4 * k4 + 2], ml[q]);
-            ml[q] = fmaf(v.w, ql[q * R + 4 * k4 + 3], ml[q]);
+            ml[q] = fmaf(vl.x, ql[q * R + 4 * k4 + 0], ml[q]);
+            ml[q] = fmaf(vl.y, ql[q * R + 4 * k4 + 1], ml[q]);
+            ml[q] = fmaf(vl.z, ql[q * R + 4 * k4 + 2], ml[q]);
+            ml[q] = fmaf(vl.w, ql[q * R + 4 * k4 + 3], ml[q]);
           }
         }
       }

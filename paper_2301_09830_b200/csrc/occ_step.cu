@@ -87,7 +87,7 @@ static size_t smem_bytes_for(const Geometry& g) {
   size_t b = (size_t)B_ROWS * R * 4;
   size_t c = orth_bytes<R>() + 2 * (size_t)B_ROWS * R * 4;
   size_t d = ((size_t)g.rs2 * R + 4 * (size_t)Cfg<R>::CPT * Cfg<R>::KS * 32) * 4;
-  size_t f = (size_t)F_ROWS * R * 4;
+  size_t f = 2 * (size_t)F_ROWS * R * 4;   // P rows + Ploc rows (DP, OCC_ORIENT_T)
   return std::max({a, b, c, d, f});
 }
 
@@ -131,12 +131,15 @@ WsLayout make_layout(const Geometry& g, int nmat) {
   off += kTraceBytes;                                      // per-CTA phase trace (occ_read_trace)
   L.p_part = off; off = al(off + (size_t)g.s1 * g.n * R * 4);
   L.q_part = off; off = al(off + (size_t)g.s2 * g.m * R * 4);
-  L.g_part = off; off = al(off + (size_t)g.ngp * np * 8);
-  L.g2_part = off; off = al(off + (size_t)g.ngp * np * 8);
-  L.xy_part = off; off = al(off + (size_t)g.ngp * 2 * R * R * 8);
+  // Gram partials: per 128 rows of the orthonormalised factor, which is the
+  // row side (n) or, with OCC_ORIENT_T, the column side (m)
+  const size_t ngp = std::max<size_t>(g.ngp, (size_t)((g.m + B_ROWS - 1) / B_ROWS));
+  L.g_part = off; off = al(off + ngp * np * 8);
+  L.g2_part = off; off = al(off + ngp * np * 8);
+  L.xy_part = off; off = al(off + ngp * 2 * R * R * 8);
   L.p_bucket = off; off = al(off + (size_t)nmat * g.n * R * 4);
   L.qw_bucket = off; off = al(off + (size_t)nmat * g.m * R * 4);
-  L.qs_bucket = off; off = al(off + (size_t)nmat * g.m * R * 4);
+  L.qs_bucket = off; off = al(off + (size_t)nmat * std::max(g.n, g.m) * R * 4);   // reduced Q (or V, OCC_ORIENT_T)
   L.v2_tail_bytes = v2_tail_bytes(g.n, g.m, R, 148);   // reused by every matrix of a multi-matrix call
   L.v2_tail = off; off = al(off + L.v2_tail_bytes);
   L.total = off;

@@ -75,6 +75,31 @@ def main():
         report(name, recon_rel=e_recon, err_rel=e_err, q_rel=q_rel, orth=orth, identical_on_ranks=same,
                ok=e_recon <= 1e-4 and e_err <= 1e-4 and same and orth <= 1e-5 and q_rel <= 1e-3)
 
+    # ------------------------------------------------------------------ DP, OCC_ORIENT_T (reading C6)
+    for flags, name in ((occ.OCC_ORIENT_T, "dp_orient_t_local_ef"),
+                        (occ.OCC_ORIENT_T | occ.OCC_EF_GLOBAL, "dp_orient_t_global_ef")):
+        n, m, r = 1536, 512, 16      # tall, like the 50257 x 3072 embedding
+        Ms = [synth.d2_gradlike(n, m, 520 + w) for w in range(world)]
+        Es = [synth.e0(n, m, 620 + w, like=Ms[w]) for w in range(world)]
+        Q0 = synth.q0(n, r, 13)      # row side with OCC_ORIENT_T
+        G = torch.from_numpy(Ms[rank]).to(dev)
+        E = torch.from_numpy(Es[rank]).to(dev)
+        Q = torch.from_numpy(Q0).to(dev)
+        P = torch.empty(m, r, device=dev)
+        occ.occ_allreduce_factors([G], [E], [Q], [P], r, 1.0 / world, flags=flags, comm=comm)
+        torch.cuda.synchronize()
+        o = oracle.dp_step(Ms, Es, Q0, scale=1.0 / world, ef_global=bool(flags & occ.OCC_EF_GLOBAL), orient_t=True)
+        A = sum(Ms[w].astype(np.float64) + Es[w] for w in range(world))
+        gs, es = gather_np(G), gather_np(E)
+        e_recon = max(rel(gs[w], o["recon"], A / world) for w in range(world))
+        e_err = max(rel(es[w], o["err"][w], Ms[w].astype(np.float64) + Es[w]) for w in range(world))
+        same = all(np.array_equal(gs[0], gs[w]) for w in range(world))
+        Ph = P.double().cpu().numpy()
+        orth = float(np.linalg.norm(Ph.T @ Ph - np.eye(r)))
+        q_rel = rel(Q.double().cpu().numpy(), o["Q"], o["Q"])
+        report(name, recon_rel=e_recon, err_rel=e_err, q_rel=q_rel, orth=orth, identical_on_ranks=same,
+               ok=e_recon <= 1e-4 and e_err <= 1e-4 and same and orth <= 1e-5 and q_rel <= 1e-3)
+
     # ------------------------------------------------------------------ PP (pairs 1 -> 0, 3 -> 2, ...)
     if world >= 2:
         n, m, r = 2048, 3072, 32      # BASELINE configs[2] shape class (8.3B hidden), shortened rows
@@ -148,6 +173,18 @@ def main():
     A = sum(g.astype(np.float64) for g in Gs)
     e2 = rel(G.double().cpu().numpy(), o["recon"], A / D)
     report("emb_compressed", recon_rel=e2, ok=e2 <= 1e-4)
+
+    # ------------------------------------------------------------------ EMB compressed as G^T (C5, reading C6)
+    G = torch.from_numpy(Gs[rank]).to(dev)
+    E = torch.zeros(V, h, device=dev)
+    Q0 = synth.q0(V, r, 12)
+    Q = torch.from_numpy(Q0).to(dev)
+    P = torch.empty(h, r, device=dev)
+    occ.occ_embed_sync(G, E, Q, P, r, 1.0 / D, comm, flags=occ.OCC_ORIENT_T)
+    torch.cuda.synchronize()
+    o = oracle.dp_step(Gs, None, Q0, scale=1.0 / D, orient_t=True)
+    e3 = rel(G.double().cpu().numpy(), o["recon"], A / D)
+    report("emb_compressed_orient_t", recon_rel=e3, ok=e3 <= 1e-4)
 
     comm.destroy()
     dist.destroy_process_group()

@@ -167,6 +167,30 @@ def test_amp_gate_rejects_collinear_factor():
     check_step(g, o, M.astype(np.float64) + e, tol=TOL32, check_factors=False)
 
 
+@pytest.mark.parametrize("bf16", [False, True])
+@pytest.mark.parametrize("multi", [False, True])
+def test_orient_t_matches_oracle(bf16, multi):
+    """OCC_ORIENT_T (reading C6): the step on A^T in A's stored layout; P is
+    m x r (orthonormal, column side), Q is n x r (row side, warm start)."""
+    n, m, r = 1000, 264, 16
+    M = synth.d2_gradlike(n, m, 81)
+    e = synth.e0(n, m, 82, like=M)
+    Q0 = synth.q0(n, r, 83)
+    flags = occ.OCC_ORIENT_T | (occ.OCC_FORCE_MULTI if multi else 0)
+    Md = to_dev(M, torch.bfloat16 if bf16 else torch.float32)
+    Ed, Qd = to_dev(e), to_dev(Q0)
+    Pd = torch.empty(m, r, device="cuda")
+    Rd = torch.empty_like(Md)
+    ws = occ.occ_compress(Md, Ed, Qd, Pd, Rd, r=r, flags=flags)
+    torch.cuda.synchronize()
+    assert occ.occ_read_stats(ws)["path"] == (2 if multi else 1)
+    M_used = Md.double().cpu().numpy()
+    o = oracle.compress_step(M_used, e, Q0, orient_t=True, out_dtype="bf16" if bf16 else "f64")
+    g = {"P_hat": Pd.double().cpu().numpy(), "Q": Qd.double().cpu().numpy(), "recon": Rd.double().cpu().numpy(),
+         "err": Ed.double().cpu().numpy()}
+    check_step(g, o, M_used + e, tol=TOLBF if bf16 else TOL32)
+
+
 def test_zero_input_all_fallbacks():
     n, m, r = 300, 264, 8
     M = np.zeros((n, m), np.float32)
