@@ -19,6 +19,8 @@ struct Geometry {
 constexpr size_t kTraceOffset = 256;
 constexpr int kTraceSlots = 48;                           // per CTA: 24 clock64 stamps, then the matching globaltimer stamps (v2::kTrStamps)
 constexpr size_t kTraceBytes = 160 * kTraceSlots * 8;     // up to 160 CTAs
+constexpr size_t kBarLinesOffset = kTraceOffset + kTraceBytes;   // v2 grid barrier: spread arrival counters
+constexpr size_t kBarLinesBytes = 8 * 128;                        // (v2::kBarLines lines of 128 B)
 
 struct WsLayout {
   size_t bar = 0, p_part = 0, q_part = 0, g_part = 0, g2_part = 0, xy_part = 0;

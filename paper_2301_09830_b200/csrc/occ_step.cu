@@ -129,6 +129,7 @@ WsLayout make_layout(const Geometry& g, int nmat) {
   size_t off = 0;
   L.bar = off; off += 256;                                 // bar[2], ctl[4], stats
   off += kTraceBytes;                                      // per-CTA phase trace (occ_read_trace)
+  off += kBarLinesBytes;                                   // v2 grid-barrier arrival lines
   L.p_part = off; off = al(off + (size_t)g.s1 * g.n * R * 4);
   L.q_part = off; off = al(off + (size_t)g.s2 * g.m * R * 4);
   // Gram partials: per 128 rows of the orthonormalised factor, which is the

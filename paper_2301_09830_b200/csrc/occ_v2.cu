@@ -43,7 +43,7 @@ __device__ __noinline__ void orth_slow(const Params2& p, Tile T, OrthW& o, float
       p.XY_band[(size_t)T.rb * 2 * R * R + q] = gg;
     }
   }
-  grid_barrier(p.bar, epoch * gridDim.x);
+  grid_barrier_spread(p.barl, epoch);
   reduce_partials<R>(p.G_band, p.nr, o, gscr);
   for (int q = tid; q < 2 * R * R; q += NT) {
     double gg = 0.0;
@@ -68,7 +68,7 @@ __device__ __noinline__ void second_pass(const Params2& p, Tile T, OrthW& o, flo
                                          unsigned epoch, bool active) {
   constexpr int RP = K<R>::RP, NP = K<R>::NP;
   if (active && T.cb == 0) band_gram<R>(ps, T.th, p.G2_band + (size_t)T.rb * NP, gscr);
-  grid_barrier(p.bar, epoch * gridDim.x);
+  grid_barrier_spread(p.barl, epoch);
   reduce_partials<R>(p.G2_band, p.nr, o, gscr);
   __syncthreads();
   if (threadIdx.x < 32) ldl_warp<R>(o, 0.0, false);
@@ -209,7 +209,7 @@ __device__ __noinline__ unsigned cold_orth_q(const Params2& p, Tile T, OrthW& o,
   __syncthreads();
   if (active) q_part_from_tmem<R, MBF>(p, T, pa, taddr_w);
   nb++;
-  grid_barrier(p.bar, nb * gridDim.x);
+  grid_barrier_spread(p.barl, nb);
   if (active) {
     const int2 cs = q_slice(T, p.nr);
     float* Qo = p.Qout + (size_t)(T.col0 + cs.x) * R;
@@ -356,6 +356,7 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
   p.XY_band = reinterpret_cast<double*>(take((size_t)pl.nr * 2 * R * R * 8));
   p.bar = p1.bar;
   p.trace = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(p1.bar) + kTraceOffset);
+  p.barl = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(p1.bar) + kBarLinesOffset);
   p.stats = p1.stats;
   p.fb_seed = p1.fb_seed;
   p.tau = p1.tau;

@@ -68,7 +68,8 @@ struct Params2 {
   double* G2_band;     // [nr][NP]
   double* XY_band;     // [nr][2 R R]
   float* Q_part;       // [nr][m][R]
-  unsigned* bar;
+  unsigned* bar;        // [0] unused here, [1] exit counter
+  unsigned* barl;       // grid_barrier_spread arrival lines (kBarLines x 32 words)
   unsigned long long* trace;   // [grid][2 kTrStamps]: clock64 stamps, then globaltimer stamps
   DevStats* stats;
   unsigned long long fb_seed;
@@ -79,19 +80,37 @@ struct Params2 {
   int debug;           // bit 0: skip phase-1 compute (streaming floor measurement only)
 };
 
-// ------------------------------------------------------------------ group grid barrier
-// grid_barrier over a sub-group of each CTA's threads (sync() is the group's
-// CTA-level barrier, thread 0 must belong to it): the CTA's other warps keep
-// working (phase 3: warp NW-1 finishes the conditioning estimates meanwhile).
-template <class Sync>
-__device__ __forceinline__ void grid_barrier_group(unsigned* ctr, unsigned target, Sync sync) {
+// ------------------------------------------------------------------ grid barrier
+// Arrivals are spread over kBarLines counters on separate 128-B lines (CTA b
+// adds to line b % kBarLines), so 148 red.release ops do not serialise on one
+// L2 line; lanes 0..kBarLines-1 of warp 0 poll one line each.  Barrier number
+// `epoch` (1, 2, ...) of the launch completes when line j holds epoch x (the
+// CTAs mapped to it).  sync() is the CTA-level barrier of the participating
+// threads (warp 0 must participate): the phase-3 compute-warp barrier lets warp
+// NW-1 keep working through it.  Ordering: bar.sync + gpu-scope release /
+// acquire, as in the single-counter barrier (occ_kernels.cuh grid_barrier).
+constexpr int kBarLines = 8;
+struct SyncBlock {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+template <class Sync = SyncBlock>
+__device__ __forceinline__ void grid_barrier_spread(unsigned* lines, unsigned epoch, Sync sync = Sync()) {
   sync();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(1u) : "memory");
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    } while (v < target);
+  if (threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
+    if (lane == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(lines + (blockIdx.x % kBarLines) * 32), "r"(1u)
+                   : "memory");
+    if (lane < kBarLines) {
+      const unsigned cnt = gridDim.x > lane ? (gridDim.x - lane + kBarLines - 1) / kBarLines : 0u;
+      const unsigned target = epoch * cnt;
+      const unsigned* ln = lines + lane * 32;
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ln) : "memory");
+      } while (v < target);
+    }
+    __syncwarp();
   }
   sync();
 }
@@ -128,9 +147,13 @@ __device__ __forceinline__ unsigned tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
+// x = hi + lo with hi an exact tf32 value (the low 13 mantissa bits masked off)
+// and lo = x - hi exact in fp32; the tensor core reads lo's top 19 bits, so
+// the split is accurate to ~2^-21 |x|.  Two ALU ops: cvt.rna.tf32.f32 is
+// emulated with ~3 integer ops per conversion on sm_100a.
 __device__ __forceinline__ void split3(float x, unsigned& hi, unsigned& lo) {
-  hi = tf32_rna(x);
-  lo = tf32_rna(x - __uint_as_float(hi));
+  hi = __float_as_uint(x) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
 }
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
   asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"

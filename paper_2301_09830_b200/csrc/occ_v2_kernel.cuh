@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   const Tile T = tile_of(p);
   const bool active = T.rb < p.nr && T.th > 0 && T.tw > 0;
   unsigned nb = 0;
-  auto gbar = [&]() { nb++; grid_barrier(p.bar, nb * gridDim.x); };
+  auto gbar = [&]() { nb++; grid_barrier_spread(p.barl, nb); };
 #ifdef OCC_TRACE
   // Instrumented build (libocc_trace.so, tools/trace.py): per-CTA phase stamps
   // and timing experiments.  The product build compiles all of it out: its
@@ -83,16 +83,22 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   uint64_t* full = mbar;
   uint64_t* empty = mbar + MAX_STAGES;
   const int sw = p.sw;
+  // one stage = SR rows of M and e: the expect_tx arrival (lane 0), then one
+  // bulk copy per row and matrix, issued by 2 SR lanes of the producer warp in
+  // one instruction (a single issuing thread caps a CTA at ~40 GB/s of 2 KB copies)
   auto issue = [&](int s) {
     const int slot = s % p.ns;
     const int r0 = s * SR, nrow = min(SR, T.th - r0);
     const unsigned rbM = (unsigned)(T.tw * esz), rbE = (unsigned)(T.tw * 4);
-    mbar_expect_tx(&full[slot], (unsigned)nrow * (rbM + (p.err_in ? rbE : 0u)));
-    for (int i = 0; i < nrow; i++) {
+    if (lane == 0) mbar_expect_tx(&full[slot], (unsigned)nrow * (rbM + (p.err_in ? rbE : 0u)));
+    __syncwarp();
+    const int i = lane >> 1;
+    if (i < nrow) {
       const size_t gi = (size_t)(T.row0 + r0 + i);
-      bulk_g2s(stM + ((size_t)(slot * SR + i) * sw) * 4,
-               reinterpret_cast<const char*>(p.M) + (gi * p.ldm + T.col0) * esz, rbM, &full[slot]);
-      if (p.err_in)
+      if ((lane & 1) == 0)
+        bulk_g2s(stM + ((size_t)(slot * SR + i) * sw) * 4,
+                 reinterpret_cast<const char*>(p.M) + (gi * p.ldm + T.col0) * esz, rbM, &full[slot]);
+      else if (p.err_in)
         bulk_g2s(stE + (size_t)(slot * SR + i) * sw, p.err_in + gi * p.lde_in + T.col0, rbE, &full[slot]);
     }
   };
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   unsigned long long wait_ns = 0;
   if (w == NW - 1) {
     // ---------------- producer
-    if (active && lane == 0) {
+    if (active) {   // the whole producer warp (copies issued by 2 SR lanes)
       for (int s = 0; s < nst; s++) {
         const int slot = s % p.ns;
         if (s >= p.ns) mbar_wait(&empty[slot], (unsigned)(((s / p.ns) - 1) & 1));
@@ -179,7 +185,11 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       for (int j = 0; j < KREG; j++)
 #pragma unroll
         for (int mt = 0; mt < MT; mt++) acc[j][mt][0] = acc[j][mt][1] = acc[j][mt][2] = acc[j][mt][3] = 0.f;
-      if constexpr (QREG) {
+      const bool x_mma = kTrace && (p.debug & 128);    // ablation experiments (trace build only)
+      const bool x_tmem = kTrace && (p.debug & 256);
+      const bool x_red = kTrace && (p.debug & 512);
+      if (x_mma) {
+      } else if constexpr (QREG) {
 #pragma unroll
         for (int j = 0; j < KREG; j++) {
           const int kk = w + NCW * j;
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
         }
       }
       // (b) TMEM: cells of row block s in this warp's column groups
-      for (int cg = w; cg < T.ncg; cg += NCW) {
+      for (int cg = w; !x_tmem && cg < T.ncg; cg += NCW) {
         const int cs = cell_slot(s, cg);
         if (cs >= TMEM_CELLS) continue;
         const int c = 16 * cg + 2 * g;
@@ -223,7 +233,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);   // this warp is done with the slot
-      {  // this warp's partial P^T for rows 8s..8s+7 -> its own slot (reduced once after the loop)
+      if (!x_red) {  // this warp's partial P^T for rows 8s..8s+7 -> its own slot (reduced once after the loop)
          // D[k][row]: c0 = (k=16mt+g, row=2t), c1 = (g, 2t+1), c2 = (g+8, 2t), c3 = (g+8, 2t+1)
         float* rw = red + ((size_t)w * nst + s) * SR * RP;
 #pragma unroll
@@ -382,7 +392,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       if (stamp) p.stats->t_ns[4] = gtimer();
       tr(9);
       nb++;
-      grid_barrier_group(p.bar, nb * gridDim.x, SyncCompute());
+      grid_barrier_spread(p.barl, nb, SyncCompute());
       tr(10);
       if (stamp) p.stats->t_ns[5] = gtimer();
 
@@ -511,7 +521,8 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
   if (tid == 0) {
     const unsigned old = atomicAdd(p.bar + 1, 1u);
-    if (old == gridDim.x - 1) {
+    if (old == gridDim.x - 1) {   // last CTA out: reset the barrier words for the next launch
+      for (int j = 0; j < kBarLines; j++) atomicExch(p.barl + j * 32, 0u);
       atomicExch(p.bar, 0u);
       atomicExch(p.bar + 1, 0u);
     }
