@@ -292,9 +292,15 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
     for (int x = tid; x < H8 * RP; x += NT) {
       const int i = x / RP, k = x % RP;
       float v = 0.f;
-      if (i < T.th && k < R) {
+      if (i < T.th && k < R) {   // the nc partials live in L2: 8 independent loads in flight (fixed order)
         const float* src = p.P_part + ((size_t)T.row0 + i) * R + k;
-        for (int c = 0; c < p.nc; c++) v += __ldcg(src + (size_t)c * p.n * R);
+        for (int c0 = 0; c0 < p.nc; c0 += 8) {
+          float u[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) u[j] = (c0 + j < p.nc) ? __ldcg(src + (size_t)(c0 + j) * p.n * R) : 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; j++) v += u[j];
+        }
       }
       ps[x] = v;
     }
@@ -327,43 +333,52 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   // general path at once; kappa > kappa_thr or amp > amp_thr is checked after
   // phase 5 when every cell is TMEM-resident (spec; the redo recomputes from
   // TMEM), else before it.
-  reduce_partials<R>(p.G_band, p.nr, o, gscr);
-  tr(6);
-  if (stamp) p.stats->t_ns[9] = gtimer();
+  // Warp groups (occ_v2_la.cuh): group A reduces G and hands it to warp NW-1
+  // (named barrier 3: A arrives, NW-1 waits), which factors it (LDL^T, the
+  // degenerate-column test) and forms Li, kappa and amp, publishing progress in
+  // o.prog (R + 1: factored, R + 2: Li ready, -1: degenerate).  Meanwhile all
+  // compute warps reduce the Q~ slice.  Then: P_hat = P Li^T, Q = Q~ Li^T in one
+  // parallel pass (reading C20; the fused Q's rounding is amplified by amp =
+  // ||S Li^T||, ~sqrt(r) for a warm-started P).  A degenerate column, a forced
+  // or needed CholQR2 pass, or amp > amp_thr take the general path.
   const int2 qs_cols = active ? q_slice(T, p.nr) : make_int2(0, 0);
   const int nqc = qs_cols.y - qs_cols.x;
   const bool force2 = p.force_two_pass != 0;
   bool deg;
   if (w == NW - 1) {
-    deg = ldl_warp<R>(o, p.tau * p.tau, true, true) != 0;
+    asm volatile("bar.sync 3, %0;" ::"r"((NWA + 1) * 32) : "memory");
+    deg = ldl_warp_unrolled<R>(o, p.tau * p.tau, true) != 0;
     trw(8);
-    if (!deg && !force2) {
-      inverse_warp<R>(o);
+    if (!deg) {
+      inverse_warp_unrolled<R>(o);
       trw(15);
     }
   } else {
-    if (active) {
+    if (in_group_a(w)) {
+      reduce_partials<R>(p.G_band, p.nr, o, gscr, group_a_index(), NWA * 32, SyncGroupA());
+      asm volatile("bar.arrive 3, %0;" ::"r"((NWA + 1) * 32) : "memory");
+      tr(6);
+      if (stamp) p.stats->t_ns[9] = gtimer();
+    }
+    if (active) {   // all compute warps (group B waits here for A's G reduce)
       strided_sum<float>(p.Q_part + (size_t)(T.col0 + qs_cols.x) * R, (size_t)p.m * R, p.nr, nqc * R,
                          reinterpret_cast<float*>(gscr), [&](int e, float v) { qsm[e] = v; }, tid, NCW * 32,
-                         SyncCompute());
+                         SyncCompute());   // (scratch first written after a compute-group barrier: A is done with it)
       tr(7);
     }
-    if (!force2 && active)
-      deg = !solve_rows_pipelined<R>(ps, H8, T.th, qsm, nqc, o, ps2, p.Qout + (size_t)(T.col0 + qs_cols.x) * R);
-    else
-      deg = !wait_prog(o, R + 1);
+    deg = !wait_prog(o, R + 2);
   }
   if (stamp) p.stats->t_ns[10] = gtimer();
   tr(5);
-  bool fused = !deg && !force2;   // uniform over the grid (every CTA factors the same G)
+  // uniform over the grid (every CTA factors the same G); warp NW-1 published
+  // kappa / amp before R + 2 (and read its own values)
+  bool fused = !deg && !force2 && !(o.kappa > p.kappa_thr) && !(o.amp > p.amp_thr);
   float* phat = ps2;
-  if (fused && !p.spec) {
+  if (fused) {
+    if (w < NCW && active)
+      apply_li<R>(ps, H8, T.th, qsm, nqc, o, ps2, p.Qout + (size_t)(T.col0 + qs_cols.x) * R, tid, NCW * 32);
+  } else {
     __syncthreads();
-    fused = !(o.kappa > p.kappa_thr || o.amp > p.amp_thr);
-  } else if (!fused) {
-    __syncthreads();
-  }
-  if (!fused) {
     nb = cold_orth_q<R, MBF>(p, T, o, ps, ps2, gscr, pa, taddr_w, nb, active, deg);
     phat = ps;
   }

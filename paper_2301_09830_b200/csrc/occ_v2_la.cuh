@@ -41,6 +41,21 @@ struct SyncAll {
 struct SyncCompute {   // the NCW compute warps 0 .. NCW-1 (named barrier 1)
   __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory"); }
 };
+// Phase-3 warp groups: A = compute warps off warp NW-1's scheduler (w % 4 != 3),
+// B = the compute warps that share it (w % 4 == 3).  Named barriers 2 and 4.
+constexpr int NWA = NCW - NCW / 4, NWB = NCW / 4;
+__device__ __forceinline__ bool in_group_a(int w) { return w < NCW && (w & 3) != 3; }
+__device__ __forceinline__ int group_a_index() {   // dense 0 .. 32 NWA - 1
+  const int w = threadIdx.x >> 5;
+  return (w - (w >> 2)) * 32 + (threadIdx.x & 31);
+}
+__device__ __forceinline__ int group_b_index() { return (threadIdx.x >> 7) * 32 + (threadIdx.x & 31); }
+struct SyncGroupA {
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 2, %0;" ::"r"(NWA * 32) : "memory"); }
+};
+struct SyncGroupB {
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 4, %0;" ::"r"(NWB * 32) : "memory"); }
+};
 
 // out[e] = sum_{u < S} src[u * stride + e], e < E, in a fixed order (deterministic),
 // by the threads x in [0, nthr) of a group synchronised by sync().  Every thread
@@ -80,17 +95,21 @@ __device__ void strided_sum(const Tv* __restrict__ src, size_t stride, int S, in
 }
 
 // G (packed upper triangle, nparts partials) -> o.L (full symmetric), o.gdiag.  All threads.
-template <int R>
-__device__ void reduce_partials(const double* __restrict__ part, int nparts, OrthW& o, double* scratch) {
+template <int R, typename Sync = SyncAll>
+__device__ void reduce_partials(const double* __restrict__ part, int nparts, OrthW& o, double* scratch,
+                                int x = threadIdx.x, int nthr = NT, Sync sync = Sync()) {
   constexpr int NP = K<R>::NP;
-  strided_sum<double>(part, NP, nparts, NP, scratch, [&](int q, double gsum) {
-    int a = 0, rem = q;
-    while (rem >= R - a) { rem -= R - a; a++; }
-    const int b = a + rem;
-    o.L[a * LD + b] = gsum;
-    o.L[b * LD + a] = gsum;
-    if (a == b) o.gdiag[a] = gsum;
-  });
+  strided_sum<double>(
+      part, NP, nparts, NP, scratch,
+      [&](int q, double gsum) {
+        int a = 0, rem = q;
+        while (rem >= R - a) { rem -= R - a; a++; }
+        const int b = a + rem;
+        o.L[a * LD + b] = gsum;
+        o.L[b * LD + a] = gsum;
+        if (a == b) o.gdiag[a] = gsum;
+      },
+      x, nthr, sync);
 }
 
 // 1/d for normal d > 0: MUFU reciprocal estimate + two Newton steps (full fp64
@@ -102,6 +121,20 @@ __device__ __forceinline__ double rcp_fast(double d) {
   r = fma(r, e, r);
   e = fma(-d, r, 1.0);
   return fma(r, e, r);
+}
+
+// ldl_warp publish protocol: o.prog is written with st.release.cta after the
+// step's shared stores (made visible to lane 0 by __syncwarp) and read with
+// ld.acquire.cta by the solvers.
+__device__ __forceinline__ void prog_release(OrthW& o, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(&o.prog)), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ int prog_acquire(const OrthW& o) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(&o.prog))
+               : "memory");
+  return v;
 }
 
 // Warp-level right-looking LDL^T of the Gram in o.L (R <= 32), square-root free
@@ -122,6 +155,9 @@ __device__ int ldl_warp(OrthW& o, double tau2, bool detect, bool publish = false
   double rr[R];
 #pragma unroll
   for (int k = 0; k < R; k++) rr[k] = (i < R) ? o.L[i * LD + k] : 0.0;
+  if (publish && R <= 16) {   // rows R..31 of o.L read as zero by solve_rows_pipelined
+    for (int x = i; x < (32 - R) * LD; x += 32) o.L[R * LD + x] = 0.0;
+  }
   int deg = 0;
 #pragma unroll 1
   for (int j = 0; j < R; j++) {
@@ -130,8 +166,9 @@ __device__ int ldl_warp(OrthW& o, double tau2, bool detect, bool publish = false
     const double d = o.col[j];
     const double gj = o.gdiag[j];
     double cv[R - 1];
-#pragma unroll
-    for (int k = 1; k < R; k++) cv[k - 1] = o.col[min(j + k, R - 1)];   // a_{j+k, j} (k > R-1-j: unused)
+    const double* cj = o.col + j;   // o.col has 32 entries: j + k <= 2R - 2 < 32 (R <= 16) or is past
+#pragma unroll                      // the active part, whose rr entries are shifted out unused
+    for (int k = 1; k < R; k++) cv[k - 1] = (R <= 16 || j + k < 32) ? cj[k] : 0.0;   // a_{j+k, j}
     if (detect && (gj == 0.0 || !(d >= tau2 * gj))) { deg = 1; break; }
     const double lij = (i > j && i < R) ? rr[0] * rcp_fast(d > 0.0 ? d : 1e-300) : 0.0;
 #pragma unroll
@@ -140,10 +177,7 @@ __device__ int ldl_warp(OrthW& o, double tau2, bool detect, bool publish = false
     if (i > j && i < R) o.L[i * LD + j] = lij;
     if (i == j) o.D[j] = d;
     __syncwarp();
-    if (publish && i == 0) {
-      __threadfence_block();
-      *reinterpret_cast<volatile int*>(&o.prog) = j + 1;
-    }
+    if (publish && i == 0) prog_release(o, j + 1);
   }
   if (!deg && i < R) {
 #pragma unroll 1
@@ -151,10 +185,7 @@ __device__ int ldl_warp(OrthW& o, double tau2, bool detect, bool publish = false
     o.dinv[i] = 1.0 / sqrt(o.D[i]);
   }
   __syncwarp();
-  if (publish && i == 0) {
-    __threadfence_block();
-    *reinterpret_cast<volatile int*>(&o.prog) = deg ? -1 : R + 1;
-  }
+  if (publish && i == 0) prog_release(o, deg ? -1 : R + 1);
   return deg;
 }
 
@@ -205,13 +236,142 @@ __device__ void inverse_warp(OrthW& o) {
   __syncwarp();
 }
 
+// The same factorisation fully unrolled (register rows, static indices): the
+// dynamic instruction count is ~35% lower than the rotated loop's (3.9k vs
+// 6.0k cycles for R = 16, tools/la_bench.cu), at ~1.2k more instructions of
+// code.  Used on the hot path, always in publish mode; same protocol and
+// results as ldl_warp.
+template <int R>
+__device__ int ldl_warp_unrolled(OrthW& o, double tau2, bool detect) {
+  const int i = threadIdx.x & 31;
+  double row[R];
+#pragma unroll
+  for (int k = 0; k < R; k++) row[k] = (i < R) ? o.L[i * LD + k] : 0.0;
+  if (R <= 16) {   // rows R..31 of o.L read as zero by solve_rows_pipelined
+    for (int x = i; x < (32 - R) * LD; x += 32) o.L[R * LD + x] = 0.0;
+  }
+  int deg = 0;
+#pragma unroll
+  for (int j = 0; j < R; j++) {
+    if (i >= j && i < R) o.col[i] = row[j];   // u_i = G_ij after the previous updates
+    __syncwarp();
+    const double d = o.col[j];
+    const double gj = o.gdiag[j];
+    if (detect && (gj == 0.0 || !(d >= tau2 * gj))) { deg = 1; break; }
+    const double rinv = rcp_fast(d > 0.0 ? d : 1e-300);
+    const double lij = row[j] * rinv;
+#pragma unroll
+    for (int k = j + 1; k < R; k++)
+      if (i >= k && i < R) row[k] = fma(-lij, o.col[k], row[k]);
+    if (i > j && i < R) {
+      row[j] = lij;
+      o.L[i * LD + j] = lij;
+    }
+    if (i == j) { o.D[j] = d; row[j] = 1.0; }
+    __syncwarp();
+    if (i == 0) prog_release(o, j + 1);
+  }
+  if (!deg && i < R) {
+#pragma unroll
+    for (int k = 0; k < R; k++) o.L[i * LD + k] = (k <= i) ? row[k] : 0.0;
+    o.dinv[i] = 1.0 / sqrt(o.D[i]);
+  }
+  __syncwarp();
+  if (i == 0) prog_release(o, deg ? -1 : R + 1);
+  return deg;
+}
+
+// inverse_warp fully unrolled (column c of L^-1 in lane c's registers): ~2.5k
+// cycles for R = 16 against ~11k for the rolled loop (tools/la_bench.cu); used
+// on the hot path, right after the factorisation.  Then publishes o.prog = R + 2.
+template <int R>
+__device__ void inverse_warp_unrolled(OrthW& o) {
+  const int c = threadIdx.x & 31;
+  double col[R];
+#pragma unroll
+  for (int i = 0; i < R; i++) {
+    double v0 = (i == c) ? 1.0 : 0.0, v1 = 0.0;   // two chains for ILP
+#pragma unroll
+    for (int k = 0; k < i; k++) {
+      if (k & 1) v1 = fma(-o.L[i * LD + k], col[k], v1);
+      else v0 = fma(-o.L[i * LD + k], col[k], v0);
+    }
+    col[i] = (i >= c && c < R) ? v0 + v1 : 0.0;
+  }
+  const double sdc = (c < R) ? sqrt(o.D[c] > 0.0 ? o.D[c] : 0.0) : 0.0;
+  double nl = 0.0, ni = 0.0;
+  if (c < R) {
+#pragma unroll
+    for (int i = 0; i < R; i++) {
+      const double v = col[i] * o.dinv[i];
+      o.Li[i * LD + c] = v;
+      ni = fma(v, v, ni);
+      const double lc = o.L[i * LD + c] * sdc;   // (L D^1/2)[i][c]
+      nl = fma(lc, lc, nl);
+    }
+  }
+  double na = (c < R) ? o.gdiag[c] * ni : 0.0;   // ||p_c||^2 * ||Li[:, c]||^2
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    nl += __shfl_xor_sync(0xffffffffu, nl, off);
+    ni += __shfl_xor_sync(0xffffffffu, ni, off);
+    na += __shfl_xor_sync(0xffffffffu, na, off);
+  }
+  if (c == 0) {
+    o.kappa = sqrt(nl) * sqrt(ni);
+    o.amp = sqrt(na);
+  }
+  __syncwarp();
+  if (c == 0) prog_release(o, R + 2);
+}
+
+// Fused path (reading C20): rows -> D^-1/2 L^-1 rows = rows Li^T with the
+// explicit Li, for the H8 rows of the P band (rows >= th zero; -> P_hat) and
+// the nqc rows of the reduced Q~ slice (-> Q).  4 threads per row, each forming
+// the outputs k = kg, kg+4, ...: independent dot products (full ILP), fp64.
+// Threads [0, nthr).
+template <int R>
+__device__ __forceinline__ void apply_li(const float* ps, int H8, int th, const float* qt, int nqc, const OrthW& o,
+                                         float* phat, float* qout, int x0, int nthr) {
+  constexpr int RP = K<R>::RP, KPT = (R + 3) / 4;
+  for (int x = x0; x < (H8 + nqc) * 4; x += nthr) {
+    const int it = x >> 2, kg = x & 3;
+    const bool isP = it < H8;
+    const float* src = isP ? ps + (size_t)it * RP : qt + (size_t)(it - H8) * R;
+    const bool zero = isP && it >= th;
+    double xv[R];
+#pragma unroll
+    for (int j = 0; j < R; j++) xv[j] = zero ? 0.0 : (double)src[j];
+    float* dst = isP ? phat + (size_t)it * RP : qout + (size_t)(it - H8) * R;
+#pragma unroll
+    for (int s2 = 0; s2 < KPT; s2++) {
+      const int k = kg + 4 * s2;
+      if (k >= R) break;
+      const double* li = o.Li + k * LD;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < R; j++) {   // Li is lower triangular: the j > k terms are zero
+        if (j & 1) a1 = fma(xv[j], li[j], a1);
+        else a0 = fma(xv[j], li[j], a0);
+      }
+      dst[k] = (float)(a0 + a1);
+    }
+  }
+}
+
 // Wait until ldl_warp (publish mode) has passed step `a` (o.prog >= a); returns
-// false if it stopped at a degenerate column.
+// false if it stopped at a degenerate column.  `seen` caches the last value
+// read, so steps the factorisation is already past cost no shared load.
+__device__ __forceinline__ bool wait_prog(const OrthW& o, int a, int& seen) {
+  while (seen < a && seen >= 0) {
+    seen = prog_acquire(o);
+    if (seen < a && seen >= 0) __nanosleep(16);
+  }
+  return seen >= 0;
+}
 __device__ __forceinline__ bool wait_prog(const OrthW& o, int a) {
-  int pv;
-  while ((pv = *reinterpret_cast<const volatile int*>(&o.prog)) < a && pv >= 0) __nanosleep(32);
-  __threadfence_block();
-  return pv >= 0;
+  int seen = 0;
+  return wait_prog(o, a, seen);
 }
 
 // Up-looking LDL^T with column substitution (slow path, thread 0): the Gram of
@@ -277,49 +437,57 @@ __device__ void band_solve(const float* ps, float* out, int nr, const OrthW& o, 
 }
 
 // Fused path (reading C20), pipelined behind ldl_warp(publish): every row x of
-// the P band (rows >= th zero; -> P_hat) and of the reduced Q~ slice (-> Q)
-// becomes D^-1/2 L^-1 x by right-looking substitution: at step a, x_a is final
-// once column a of L is (o.prog > a), and x_{a+k} -= l_{a+k,a} x_a.  The
-// registers are shifted like ldl_warp's: xr[k] holds x_{a+k}; the finished x_a
-// enters at xr[R-1] and shifts left with the rest (its l is 0), so after R steps
-// xr[k] = x_k.  Rows are spread over the compute warps that do not share warp
-// NW-1's scheduler (w % 4 != 3), so the spinning leaves the factorisation's
-// issue slots alone.  Returns false (writes nothing) if the factorisation
-// stopped at a degenerate column.
+// src ([nrows][ld]; rows >= nvalid zero) becomes D^-1/2 L^-1 x (-> dst [.][dld])
+// by right-looking substitution: at step a, x_a is final once column a of L is
+// (o.prog > a), and x_{a+k} -= l_{a+k,a} x_a.  The registers are shifted like
+// ldl_warp's: xr[k] holds x_{a+k}; the finished x_a enters at xr[R-1] and
+// shifts left with the rest (its l is 0: rows R.. of o.L are zero), so after R
+// steps xr[k] = x_k.  One row per thread x of the calling group (nthr threads).
+// Returns false (writes nothing) if the factorisation stopped at a degenerate
+// column.
 template <int R>
-__device__ __forceinline__ bool solve_rows_pipelined(const float* ps, int H8, int th, const float* qt, int nqc,
-                                                     const OrthW& o, float* phat, float* qout) {
-  constexpr int RP = K<R>::RP;
-  const int w = threadIdx.x >> 5;
+__device__ __forceinline__ bool solve_rows_pipelined(const float* src, int ld, int nrows, int nvalid, float* dst,
+                                                     int dld, const OrthW& o, int x, int nthr) {
   bool ok = true;
-  if ((w & 3) != 3) {
-    const int slot = (w - (w >> 2)) * 32 + (threadIdx.x & 31);   // dense index over the solver warps
-    constexpr int NSOLVE = (NCW - NCW / 4) * 32;
-    for (int it = slot; it < H8 + nqc; it += NSOLVE) {
-      const bool isP = it < H8;
-      const float* src = isP ? ps + (size_t)it * RP : qt + (size_t)(it - H8) * R;
-      const bool zero = isP && it >= th;
-      double xr[R];
+  int seen = 0;
+  for (int it = x; it < nrows; it += nthr) {
+    const float* s = src + (size_t)it * ld;
+    const bool zero = it >= nvalid;
+    double xr[R];
 #pragma unroll
-      for (int k = 0; k < R; k++) xr[k] = zero ? 0.0 : (double)src[k];
+    for (int k = 0; k < R; k++) xr[k] = zero ? 0.0 : (double)s[k];
+    // column a of L (from the diagonal down) is loaded during step a - 1 when
+    // the factorisation is already past it, so the loads' latency overlaps the
+    // previous step's FMAs instead of sitting in front of each FMA
+    auto load_col = [&](int a, double (&lv)[R - 1]) {
+      const double* la = o.L + a * (LD + 1);
+#pragma unroll
+      for (int k = 1; k < R; k++) lv[k - 1] = (R <= 16 || a + k < 32) ? la[k * LD] : 0.0;
+    };
+    double lv[R - 1];
+    bool have = false;
 #pragma unroll 1
-      for (int a = 0; a < R; a++) {
-        if (!wait_prog(o, a + 1)) { ok = false; break; }
-        const double xa = xr[0];
-        double lv[R - 1];
-#pragma unroll
-        for (int k = 1; k < R; k++) lv[k - 1] = (a + k < R) ? o.L[(a + k) * LD + a] : 0.0;
-#pragma unroll
-        for (int k = 1; k < R; k++) xr[k - 1] = fma(-lv[k - 1], xa, xr[k]);
-        xr[R - 1] = xa;
+    for (int a = 0; a < R; a++) {
+      if (!have) {
+        if (!wait_prog(o, a + 1, seen)) { ok = false; break; }
+        load_col(a, lv);
       }
-      if (!ok || !wait_prog(o, R + 1)) { ok = false; break; }
-      float* dst = isP ? phat + (size_t)it * RP : qout + (size_t)(it - H8) * R;
+      const double xa = xr[0];
+      double cur[R - 1];
 #pragma unroll
-      for (int k = 0; k < R; k++) dst[k] = (float)(xr[k] * o.dinv[k]);
+      for (int k = 0; k < R - 1; k++) cur[k] = lv[k];
+      have = a + 1 < R && seen >= a + 2;   // next column already final: prefetch it now
+      if (have) load_col(a + 1, lv);
+#pragma unroll
+      for (int k = 1; k < R; k++) xr[k - 1] = fma(-cur[k - 1], xa, xr[k]);
+      xr[R - 1] = xa;
     }
+    if (!ok || !wait_prog(o, R + 1, seen)) { ok = false; break; }
+    float* d = dst + (size_t)it * dld;
+#pragma unroll
+    for (int k = 0; k < R; k++) d[k] = (float)(xr[k] * o.dinv[k]);
   }
-  return ok && wait_prog(o, R + 1);
+  return ok && wait_prog(o, R + 1, seen);
 }
 
 // Fused path (reading C20): rows x -> D^-1/2 L^-1 x by forward substitution

@@ -10,8 +10,8 @@ from workloads import synth
 
 S = 24   # stamps per CTA (kTrStamps)
 SEG = [("phase1", 0, 1), ("B1 wait", 1, 2), ("ph2 w0: Pband + Q~part", 2, 3), ("ph2 w15: Pband + gram", 2, 14),
-       ("B2 (w0 arrive -> release)", 3, 4), ("G reduce", 4, 6), ("w15 LDL", 6, 8), ("w0 Q~ reduce", 6, 7),
-       ("w0 solve done (after Q~)", 7, 5), ("w15 inverse (off path)", 8, 15), ("general path (if any)", 5, 12),
+       ("B2 (w0 arrive -> release)", 3, 4), ("grpA G reduce", 4, 6), ("w15 LDL (after G)", 6, 8), ("Q~ reduce (after G)", 6, 7),
+       ("Li ready (after G)", 6, 5), ("w15 inverse", 8, 15), ("apply Li (or general path)", 5, 12),
        ("tables", 12, 13), ("B3 wait", 9, 10), ("phase5", 10, 11), ("p5: Q prefetch", 10, 16), ("p5: 1st tmem ld", 16, 17),
        ("p5: 1st MMAs", 17, 18), ("p5: 1st stores", 18, 19), ("p5: rest of 1st cg", 19, 20), ("p5: other cg", 20, 11)]
 
