@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   OrthW& o = *reinterpret_cast<OrthW*>(sm + p.off_orth);
   uint4* pa = reinterpret_cast<uint4*>(sm + p.off_pa);   // [nrblk][MT][32][2] (hi, lo)
   uint4* pb = reinterpret_cast<uint4*>(sm + p.off_pb);   // [nrblk][KS5][32]   (h0, h1, l0, l1)
-  float* qsm = reinterpret_cast<float*>(sm + p.off_qsm);   // phase 3: Q~ slice; phase 5: [tw][R] Q of the tile
+  float* qsm = reinterpret_cast<float*>(sm + p.off_qsm);   // phase 3: the reduced Q~ slice
   if (tid == 0) o.prog = 0;   // ldl_warp publish protocol (phase 3; every CTA, active or not)
   if (active) {
     for (int x = tid; x < H8 * RP; x += NT) {
@@ -412,31 +412,33 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       if (stamp) p.stats->t_ns[5] = gtimer();
 
       // ---------------------------------------------------------- phase 5 (compute warps)
-      if (active) {
-        for (int x = tid; x < T.tw * R; x += NCW * 32) qsm[x] = __ldcg(p.Qout + (size_t)T.col0 * R + x);
-      }
-      SyncCompute()();
+      // The A operand Q (M = columns 2g | 2g+1, K = rank) of a column group is
+      // used by exactly one lane: it is loaded straight from L2 (no staging, no
+      // CTA barrier), the next column group's values while this one computes.
       tr(16);
       if (active) {
+        auto load_q = [&](int cg, float (&qv)[KS5][4]) {
+          const int cl = 16 * cg + 2 * g;
+          const bool okA = cg < T.ncg && cl < T.tw, okB = cg < T.ncg && cl + 1 < T.tw;
+          const float* qa_ = p.Qout + (size_t)(T.col0 + cl) * R;
+#pragma unroll
+          for (int ks = 0; ks < KS5; ks++) {
+            const int k0 = 8 * ks + t;
+            qv[ks][0] = (okA && k0 < R) ? __ldcg(qa_ + k0) : 0.f;
+            qv[ks][1] = (okB && k0 < R) ? __ldcg(qa_ + R + k0) : 0.f;
+            qv[ks][2] = (okA && k0 + 4 < R) ? __ldcg(qa_ + k0 + 4) : 0.f;
+            qv[ks][3] = (okB && k0 + 4 < R) ? __ldcg(qa_ + R + k0 + 4) : 0.f;
+          }
+        };
+        float qnext[KS5][4];
+        load_q(w, qnext);
         for (int cg = w; cg < T.ncg; cg += NCW) {
           unsigned qh[KS5][4], ql[KS5][4];
-          {  // A operand Q (M = columns 2g | 2g+1, K = rank)
-            const int cl = 16 * cg + 2 * g;
-            const bool okA = cl < T.tw, okB = cl + 1 < T.tw;
-            const float* qa_ = qsm + (size_t)cl * R;
 #pragma unroll
-            for (int ks = 0; ks < KS5; ks++) {
-              const int k0 = 8 * ks + t;
-              const float a0 = (okA && k0 < R) ? qa_[k0] : 0.f;
-              const float a1 = (okB && k0 < R) ? qa_[R + k0] : 0.f;
-              const float a2 = (okA && k0 + 4 < R) ? qa_[k0 + 4] : 0.f;
-              const float a3 = (okB && k0 + 4 < R) ? qa_[R + k0 + 4] : 0.f;
-              split3(a0, qh[ks][0], ql[ks][0]);
-              split3(a1, qh[ks][1], ql[ks][1]);
-              split3(a2, qh[ks][2], ql[ks][2]);
-              split3(a3, qh[ks][3], ql[ks][3]);
-            }
-          }
+          for (int ks = 0; ks < KS5; ks++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) split3(qnext[ks][q], qh[ks][q], ql[ks][q]);
+          load_q(cg + NCW, qnext);
           for (int rb0 = 0; rb0 < T.nrblk; rb0 += 4) {
             float v16[16];
             const int cs0 = cell_slot(rb0, cg);
