@@ -6,9 +6,13 @@
 N = 1: the 1-GPU compress+decompress step (occ_compress: a1-a9) on
 BASELINE.json configs[1], the GPT-2.5B-shaped inter-stage tensor
 (1024 tokens x micro-batch 4) x 1920 hidden = 4096 x 1920 fp32 at rank 16.
-N > 1 (torchrun, one rank per GPU): weak scaling of the data-parallel step
-(occ_allreduce_factors: every rank compresses its own 4096 x 1920 gradient,
-ncclAllReduce of P then of Q over NVLink).
+N > 1 (torchrun, one rank per GPU): weak scaling of the pipeline backward link
+in its 1F1B steady state (concurrent sender -> receiver
+pairs), as a ring: every rank compresses its own 4096 x 1920 gradient and
+sends the factors to rank - 1 while receiving rank + 1's factors and
+decompressing them (occ_sendrecv_factors, one NCCL group over NVLink).
+--mode dp instead runs the data-parallel step (occ_allreduce_factors:
+ncclAllReduce of P then of Q).
 --impl reference: the fp64 CPU oracle (oracle/) timed on the host cores on the
 same workload (the reference arm of this paper-only tier; rank 0 only).
 
@@ -157,6 +161,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-target", action="store_true", help="skip the 1024x3072 north-star line")
+    ap.add_argument("--mode", default="pp", choices=["pp", "dp"],
+                    help="N > 1: pipeline ring (occ_sendrecv_factors, default) or data-parallel allreduce")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -194,22 +200,31 @@ def main():
 
     comm = occ.Comm.from_process_group() if world > 1 else None
 
-    def bench_shape(n, m, steps, warmup, dp):
+    mode = "1gpu" if world == 1 else args.mode
+    dp = mode == "dp"
+    snd_peer, rcv_peer = (rank - 1) % world, (rank + 1) % world   # pp ring
+
+    def bench_shape(n, m, steps, warmup, mode):
+        dp = mode == "dp"
         M, e, Q0 = make_inputs(n, m, seed=2000 + 10 * rank)
         Md = torch.from_numpy(M).to(dev)
         Ed = torch.from_numpy(e).to(dev)
         Qd = torch.from_numpy(Q0).to(dev)
         Pd = torch.empty(n, RANK, device=dev)
-        Rd = torch.empty_like(Md)
+        Rd = torch.empty_like(Md)            # M' (1gpu) / the received stage's M' (pp)
+        Pr = torch.empty(n, RANK, device=dev)
+        Qr = torch.empty(m, RANK, device=dev)
         ws = occ.alloc_workspace(n, m, RANK, device=dev)
         Mkeep = Md.clone()
 
         def step():
             if dp:
                 Md.copy_(Mkeep)   # G is overwritten in place by M'; restored outside the timing
-            if dp:
                 return lambda: occ.occ_allreduce_factors([Md], [Ed], [Qd], [Pd], RANK, 1.0 / world,
                                                          comm=comm, ws=ws)
+            if mode == "pp":
+                return lambda: occ.occ_sendrecv_factors(Md, Ed, Qd, Pd, RANK, snd_peer, Rd, Pr, Qr, rcv_peer,
+                                                        comm, ws=ws)
             return lambda: occ.occ_compress(Md, Ed, Qd, Pd, Rd, r=RANK, ws=ws)
 
         for _ in range(warmup):
@@ -240,11 +255,10 @@ def main():
         ms = tot.item() / steps
         stats = occ.occ_read_stats(ws)
         return {"ms": ms, "times": times, "clocks": sampler.summary(), "stats": stats,
-                "bufs": (Md, Ed, Qd, Pd, Rd, ws, Mkeep)}
+                "bufs": (Md, Ed, Qd, Pd, Rd, ws, Mkeep, Pr, Qr)}
 
-    dp = world > 1
     n, m = N_ROWS, N_COLS
-    res = bench_shape(n, m, args.steps, args.warmup, dp)
+    res = bench_shape(n, m, args.steps, args.warmup, mode)
     ms = res["ms"]
     value = world * n * m * 4 / (ms * 1e-3) / 1e9               # GB/s uncompressed, whole job
     ab = alg_bytes(n, m)
@@ -252,9 +266,11 @@ def main():
     launches_per_step = 1 if res["stats"]["path"] in (1, 3) else 9
     if dp:
         launches_per_step = 3
+    elif mode == "pp":
+        launches_per_step = 2   # fused compress + decompress (NCCL's send/recv kernels are not ours)
 
     # e2e through the public API with HOST buffers: H2D of M, the step, D2H of M'
-    Md, Ed, Qd, Pd, Rd, ws, Mkeep = res["bufs"]
+    Md, Ed, Qd, Pd, Rd, ws, Mkeep, Pr, Qr = res["bufs"]
     Mh = torch.from_numpy(make_inputs(n, m, seed=2000 + 10 * rank)[0]).pin_memory()
     Rh = torch.empty(n, m, dtype=torch.float32).pin_memory()
     e2e_steps = max(3, min(args.steps, 20))
@@ -267,6 +283,9 @@ def main():
         if dp:
             occ.occ_allreduce_factors([Md], [Ed], [Qd], [Pd], RANK, 1.0 / world, comm=comm, ws=ws)
             Rh.copy_(Md, non_blocking=True)
+        elif mode == "pp":
+            occ.occ_sendrecv_factors(Md, Ed, Qd, Pd, RANK, snd_peer, Rd, Pr, Qr, rcv_peer, comm, ws=ws)
+            Rh.copy_(Rd, non_blocking=True)
         else:
             occ.occ_compress(Md, Ed, Qd, Pd, Rd, r=RANK, ws=ws)
             Rh.copy_(Rd, non_blocking=True)
@@ -300,18 +319,41 @@ def main():
         ct = torch.tensor([c0.elapsed_time(c1) / reps * 1e3], dtype=torch.float64, device=dev)
         dist.all_reduce(ct, op=dist.ReduceOp.MAX)
         comm_us = ct.item()
+    elif mode == "pp":   # the grouped factor send/recv alone (P n x r + Q m x r each way)
+        bufs = [torch.zeros(n * RANK, device=dev), torch.zeros(m * RANK, device=dev),
+                torch.zeros(n * RANK, device=dev), torch.zeros(m * RANK, device=dev)]
+
+        def xchg():
+            ops = [dist.P2POp(dist.isend, bufs[0], snd_peer), dist.P2POp(dist.isend, bufs[1], snd_peer),
+                   dist.P2POp(dist.irecv, bufs[2], rcv_peer), dist.P2POp(dist.irecv, bufs[3], rcv_peer)]
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for _ in range(5):
+            xchg()
+        torch.cuda.synchronize()
+        dist.barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 50
+        c0.record()
+        for _ in range(reps):
+            xchg()
+        c1.record()
+        torch.cuda.synchronize()
+        ct = torch.tensor([c0.elapsed_time(c1) / reps * 1e3], dtype=torch.float64, device=dev)
+        dist.all_reduce(ct, op=dist.ReduceOp.MAX)
+        comm_us = ct.item()
 
     # north-star target T on one GPU (reported beside the headline)
     target = None
-    if not args.no_target and not dp:
-        t = bench_shape(T_ROWS, T_COLS, args.steps, args.warmup, False)
+    if not args.no_target and world == 1:
+        t = bench_shape(T_ROWS, T_COLS, args.steps, args.warmup, "1gpu")
         tab = alg_bytes(T_ROWS, T_COLS)
         target = {"workload": "north-star T: 1024 x 3072 fp32, rank 16, 1 GPU", "ms_per_step": t["ms"],
                   "value": T_ROWS * T_COLS * 4 / (t["ms"] * 1e-3) / 1e9, "unit": "GB/s",
                   "roofline_frac": tab / (t["ms"] * 1e-3) / 1e9 / hbm_peak}
 
     cpu = None
-    if rank == 0 and not dp and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, done = run_oracle(n, m, 1000, 12.0)
         cpu = {"value": n * m * 4 / dt / 1e9, "unit": "GB/s", "cores": cpu_threads(), "kind": "oracle",
                "sample": f"{done} oracle steps (NumPy fp64, ~12 s budget) of the same {n}x{m} r={RANK} workload"}
@@ -320,7 +362,7 @@ def main():
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(f"{n}x{m}x{RANK}" + ("_dp" if dp else ""))
+            traffic = json.load(open(tf)).get(f"{n}x{m}x{RANK}" + ("" if mode == "1gpu" else "_" + mode))
         except Exception:
             traffic = None
 
@@ -329,13 +371,18 @@ def main():
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD if not dp else WORKLOAD + f"; data-parallel allreduce of P and Q over {world} ranks",
+            "config": {"workload": WORKLOAD + {"1gpu": "",
+                                                "pp": f"; pipeline backward link, ring of {world} stages: compress + send factors to rank-1, receive rank+1's factors + decompress (1F1B steady state)",
+                                                "dp": f"; data-parallel allreduce of P and Q over {world} ranks"}[mode],
                        "n": n, "m": m, "rank": RANK, "M_dtype": "f32",
-                       "parallelism": f"dp{world}" if dp else "1gpu", "l2": "flushed before every step",
+                       "parallelism": {"1gpu": "1gpu", "pp": f"pp-ring{world}", "dp": f"dp{world}"}[mode],
+                       "l2": "flushed before every step",
                        "path": {1: "v1 fused persistent kernel", 3: "fused TMEM-resident persistent kernel"}.get(res["stats"]["path"], "per-phase launches")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "alg_bytes_per_launch": ab, "kernel": "occ_step_kernel (fused)" if not dp else "step (3 launches + 2 NCCL)"},
+                         "alg_bytes_per_launch": ab,
+                         "kernel": {"1gpu": "occ_v2_kernel (fused step)", "pp": "step (fused compress + NCCL send/recv + decompress)",
+                                    "dp": "step (3 launches + 2 NCCL allreduces)"}[mode]},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,

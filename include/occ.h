@@ -151,6 +151,17 @@ occ_status occ_send_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r,
 occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, uint32_t flags,
                             occ_comm pp, cudaStream_t stream);
 
+/* Pipeline steady state (1F1B, PAPER.md:331-337 / 386): this stage compresses
+ * its backward gradient M (occ_compress without recon) and sends (P, Q) to
+ * send_peer while it receives the next stage's factors into (Prcv, Qrcv) from
+ * recv_peer and decompresses them into out (occ_decompress).  The sends and
+ * receives form ONE NCCL group, so a ring of stages cannot deadlock.
+ * send_peer / recv_peer = -1 skip that side (the pipeline ends).  Shapes as
+ * occ_send_factors / occ_recv_factors (out is recv_peer's matrix shape). */
+occ_status occ_sendrecv_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, int send_peer,
+                                occ_mat out, occ_mat Prcv, occ_mat Qrcv, int recv_peer, uint32_t flags,
+                                occ_comm pp, void* ws, size_t ws_bytes, cudaStream_t stream);
+
 /* Fused embedding synchronisation over the 2D-rank group `emb` (PAPER.md:
  * 598-618).  r == 0: one dense allreduce-sum of scale*G in place (lossless FE).
  * r > 0: occ_allreduce_factors on the group (compressed FE, reading C14). */

@@ -285,7 +285,9 @@ occ_status occ_decompress(occ_mat P, occ_mat Q, occ_mat out, cudaStream_t stream
   p.recon = out.ptr;
   p.ldr = out.ld;
   p.r_bf16 = out.dtype == OCC_BF16;
-  cudaError_t e = run_decompress(p, r, stream);
+  cudaError_t e = want_v1() ? cudaErrorNotSupported
+                            : run_v2_decompress(p.P, p.Qrec, p.recon, p.ldr, p.n, p.m, r, p.r_bf16 != 0, stream);
+  if (e == cudaErrorNotSupported) e = run_decompress(p, r, stream);   // r = 64 (and OCC_PATH=v1)
   return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_decompress launch");
 }
 
@@ -453,6 +455,40 @@ occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, 
   ncclRecv(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream);
   if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclRecv(P,Q)");
   return ot ? occ_decompress(Q, P, out, stream) : occ_decompress(P, Q, out, stream);
+}
+
+occ_status occ_sendrecv_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, int send_peer, occ_mat out,
+                                occ_mat Prcv, occ_mat Qrcv, int recv_peer, uint32_t flags, occ_comm pp, void* ws,
+                                size_t ws_bytes, cudaStream_t stream) {
+  if (!pp) return fail(OCC_ERR_INVALID_ARG, "pp communicator is null");
+  const bool snd = send_peer >= 0, rcv = recv_peer >= 0;
+  if (snd && (send_peer >= pp->nranks || send_peer == pp->rank)) return fail(OCC_ERR_INVALID_ARG, "bad send_peer %d", send_peer);
+  if (rcv && (recv_peer >= pp->nranks || recv_peer == pp->rank)) return fail(OCC_ERR_INVALID_ARG, "bad recv_peer %d", recv_peer);
+  const bool ot = (flags & OCC_ORIENT_T) != 0;
+  if (rcv) {
+    if (!out.ptr) return fail(OCC_ERR_INVALID_ARG, "out: null pointer");
+    occ_status s = check_view(Prcv, "Prcv", ot ? out.cols : out.rows, r, true, true);
+    if (s) return s;
+    if ((s = check_view(Qrcv, "Qrcv", ot ? out.rows : out.cols, r, true, true))) return s;
+  }
+  if (snd) {
+    occ_mat none = {nullptr, 0, 0, 0, M.dtype};
+    occ_status s = occ_compress(M, err, Q, P, none, r, flags, ws, ws_bytes, stream);
+    if (s) return s;
+  }
+  ncclResult_t nr;
+  if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
+  if (snd) {
+    ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, send_peer, pp->comm, stream);
+    ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, send_peer, pp->comm, stream);
+  }
+  if (rcv) {
+    ncclRecv(Prcv.ptr, (size_t)Prcv.rows * r, ncclFloat, recv_peer, pp->comm, stream);
+    ncclRecv(Qrcv.ptr, (size_t)Qrcv.rows * r, ncclFloat, recv_peer, pp->comm, stream);
+  }
+  if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclSendRecv(P,Q)");
+  if (!rcv) return OCC_OK;
+  return ot ? occ_decompress(Qrcv, Prcv, out, stream) : occ_decompress(Prcv, Qrcv, out, stream);
 }
 
 occ_status occ_embed_sync(occ_mat G, occ_mat err, occ_mat Q, occ_mat P, int r, float scale, uint32_t flags,

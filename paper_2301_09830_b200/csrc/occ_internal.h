@@ -36,6 +36,10 @@ cudaError_t run_phases(const Params& p, const Geometry& g, int ph0, int ph1, boo
 cudaError_t run_decompress(const Params& p, int r, cudaStream_t st);
 size_t v2_tail_bytes(int64_t n, int64_t m, int r, int sms);
 cudaError_t run_v2(const Params& p, int r, void* ws_tail, size_t tail_avail, int sms, cudaStream_t st);
+// out = round(P Q^T) with the fused kernel's phase-5 arithmetic (bit-identical
+// to the sender's reconstruction, reading C8); cudaErrorNotSupported if r > 32.
+cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r, bool bf16,
+                              cudaStream_t st);
 cudaError_t run_init_q(float* q, int64_t rows, int r, int64_t ld, uint64_t seed, cudaStream_t st);
 
 }  // namespace occ

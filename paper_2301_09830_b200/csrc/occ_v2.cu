@@ -221,6 +221,83 @@ __device__ __noinline__ unsigned cold_orth_q(const Params2& p, Tile T, OrthW& o,
 
 #include "occ_v2_kernel.cuh"
 
+// ------------------------------------------------------------------ decompress
+// out = round(P Q^T) (receiver side, occ_decompress) with exactly the fused
+// kernel's phase-5 arithmetic: the same 3-term TF32 split of the same fp32
+// P_hat and Q values, the same fragments and the same MMA order, so the
+// receiver's M' is bit-identical to the M' the sender's e_new was taken
+// against (reading C8).  Work item = one warp x one 16-column group x 8 row
+// blocks; the Q fragment is loaded once per item.
+template <int R, bool BF>
+__global__ void __launch_bounds__(256) occ_v2_decompress_kernel(const float* __restrict__ P, const float* __restrict__ Q,
+                                                                void* __restrict__ out, long long ldo, int n, int m) {
+  constexpr int KS5 = K<R>::KS5, RBI = 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int ncg = (m + 15) / 16, nrb = (n + 7) / 8;
+  const int nitems = ncg * ((nrb + RBI - 1) / RBI);
+  for (int item = blockIdx.x * 8 + warp; item < nitems; item += gridDim.x * 8) {
+    const int cg = item % ncg, rb0 = (item / ncg) * RBI;
+    unsigned qh[KS5][4], ql[KS5][4];
+    {  // A operand Q (M = columns 2g | 2g+1, K = rank), as in phase 5
+      const int cl = 16 * cg + 2 * g;
+      const bool okA = cl < m, okB = cl + 1 < m;
+      const float* qa_ = Q + (size_t)cl * R;
+#pragma unroll
+      for (int ks = 0; ks < KS5; ks++) {
+        const int k0 = 8 * ks + t;
+        split3((okA && k0 < R) ? __ldg(qa_ + k0) : 0.f, qh[ks][0], ql[ks][0]);
+        split3((okB && k0 < R) ? __ldg(qa_ + R + k0) : 0.f, qh[ks][1], ql[ks][1]);
+        split3((okA && k0 + 4 < R) ? __ldg(qa_ + k0 + 4) : 0.f, qh[ks][2], ql[ks][2]);
+        split3((okB && k0 + 4 < R) ? __ldg(qa_ + R + k0 + 4) : 0.f, qh[ks][3], ql[ks][3]);
+      }
+    }
+    // the B operand (P_hat^T, N = rows n/2 + 4(n&1)) of all RBI row blocks, loaded
+    // up front so the L2 latency is paid once per item, not once per row block
+    float pf[RBI][KS5][2];
+#pragma unroll
+    for (int j = 0; j < RBI; j++) {
+      const int rn = 8 * (rb0 + j) + (g >> 1) + 4 * (g & 1);
+#pragma unroll
+      for (int ks = 0; ks < KS5; ks++) {
+        const int k = 8 * ks + t;
+        pf[j][ks][0] = (rn < n && k < R) ? __ldg(P + (size_t)rn * R + k) : 0.f;
+        pf[j][ks][1] = (rn < n && k + 4 < R) ? __ldg(P + (size_t)rn * R + k + 4) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RBI; j++) {
+      const int rblk = rb0 + j;
+      if (rblk >= nrb) break;
+      float mr[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < KS5; ks++) {
+        unsigned h0, l0, h1, l1;
+        split3(pf[j][ks][0], h0, l0);
+        split3(pf[j][ks][1], h1, l1);
+        mma3(mr, qh[ks], ql[ks], h0, h1, l0, l1);
+      }
+      // mr: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
+      const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
+      const int rows[2] = {r, r + 4};
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        if (rows[h] >= n || c >= m) continue;
+        const size_t o0 = (size_t)rows[h] * ldo + c;
+        const float v0 = mr[h], v1 = mr[2 + h];
+        if (BF) {
+          __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(out) + o0;
+          if (c + 1 < m) *reinterpret_cast<__nv_bfloat162*>(d) = __floats2bfloat162_rn(v0, v1);
+          else d[0] = __float2bfloat16_rn(v0);
+        } else {
+          float* d = reinterpret_cast<float*>(out) + o0;
+          if (c + 1 < m) *reinterpret_cast<float2*>(d) = make_float2(v0, v1);
+          else d[0] = v0;
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host side
 struct Plan2 {
   bool ok = false;
@@ -417,6 +494,22 @@ size_t v2_tail_bytes(int64_t n, int64_t m, int r, int sms) {
 #undef V2T
   }
   return 0;
+}
+
+cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r, bool bf16,
+                              cudaStream_t st) {
+  const int items = ((m + 15) / 16) * (((n + 7) / 8 + 7) / 8);
+  const int grid = std::max(1, std::min((items + 7) / 8, 148 * 8));
+  switch (r) {
+#define V2D(RR)                                                                                            \
+  case RR:                                                                                                 \
+    if (bf16) v2::occ_v2_decompress_kernel<RR, true><<<grid, 256, 0, st>>>(P, Q, out, ldo, n, m);          \
+    else v2::occ_v2_decompress_kernel<RR, false><<<grid, 256, 0, st>>>(P, Q, out, ldo, n, m);              \
+    return cudaGetLastError();
+    V2D(4) V2D(8) V2D(16) V2D(32)
+#undef V2D
+  }
+  return cudaErrorNotSupported;
 }
 
 cudaError_t run_v2(const Params& p, int r, void* ws_tail, size_t tail_avail, int sms, cudaStream_t st) {

@@ -73,6 +73,7 @@ def lib():
                                    ctypes.c_size_t, vp], c_int),
         "occ_send_factors": ([M, M, M, M, c_int, c_int, u32, vp, vp, ctypes.c_size_t, vp], c_int),
         "occ_recv_factors": ([M, M, M, c_int, c_int, u32, vp, vp], c_int),
+        "occ_sendrecv_factors": ([M, M, M, M, c_int, c_int, M, M, M, c_int, u32, vp, vp, ctypes.c_size_t, vp], c_int),
         "occ_embed_sync": ([M, M, M, M, c_int, ctypes.c_float, u32, vp, vp, ctypes.c_size_t, vp], c_int),
         "occ_get_unique_id": ([ctypes.c_char_p], c_int),
         "occ_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, c_int, c_int], c_int),
@@ -184,6 +185,19 @@ def occ_send_factors(M, err, Q, P, r: int, peer: int, comm: "Comm", flags: int =
 def occ_recv_factors(out, P, Q, r: int, peer: int, comm: "Comm", flags: int = 0, stream=None):
     _check(lib().occ_recv_factors(mat(out), mat(P), mat(Q), r, peer, flags, comm.handle, _stream(stream)),
            "occ_recv_factors")
+
+
+def occ_sendrecv_factors(M, err, Q, P, r: int, send_peer: int, out, Prcv, Qrcv, recv_peer: int, comm: "Comm",
+                         flags: int = 0, ws=None, stream=None):
+    """PP steady state: compress M and send (P, Q) to send_peer while receiving
+    recv_peer's factors and decompressing them into out (one NCCL group)."""
+    if send_peer >= 0 and ws is None:
+        ws = alloc_workspace(M.shape[0], M.shape[1], r, device=M.device)
+    _check(lib().occ_sendrecv_factors(mat(M) if send_peer >= 0 else mat(None), mat(err), mat(Q), mat(P), r, send_peer,
+                                      mat(out), mat(Prcv), mat(Qrcv), recv_peer, flags, comm.handle,
+                                      ws.data_ptr() if ws is not None else None,
+                                      ws.numel() if ws is not None else 0, _stream(stream)), "occ_sendrecv_factors")
+    return ws
 
 
 def occ_embed_sync(G, err, Q, P, r: int, scale: float, comm: Optional["Comm"], flags: int = 0, ws=None,

@@ -147,6 +147,33 @@ def main():
         else:
             ok = ok and bool(flags_t.item())
 
+    # ------------------------------------------------------------------ PP ring (1F1B steady state)
+    # every rank compresses its own gradient and sends the factors to rank - 1
+    # while receiving rank + 1's and decompressing them (occ_sendrecv_factors)
+    if world >= 2:
+        n, m, r = 1024, 3072, 16      # north-star target T
+        mats = [synth.d2_gradlike(n, m, 1100 + w) for w in range(world)]
+        errs = [synth.e0(n, m, 1200 + w, like=mats[w]) for w in range(world)]
+        Q0 = synth.q0(m, r, 17)
+        Md, Ed, Qd = (torch.from_numpy(x).to(dev) for x in (mats[rank], errs[rank], Q0))
+        Pd = torch.empty(n, r, device=dev)
+        out = torch.empty(n, m, device=dev)
+        Pr, Qr = torch.empty(n, r, device=dev), torch.empty(m, r, device=dev)
+        snd, rcv = (rank - 1) % world, (rank + 1) % world
+        occ.occ_sendrecv_factors(Md, Ed, Qd, Pd, r, snd, out, Pr, Qr, rcv, comm)
+        own = torch.empty(n, m, device=dev)
+        occ.occ_decompress(Pd, Qd, own)          # what this rank's residual assumes
+        torch.cuda.synchronize()
+        owns = gather_np(own)
+        o = oracle.compress_step(mats[rcv], errs[rcv], Q0)
+        A = mats[rcv].astype(np.float64) + errs[rcv]
+        got = out.double().cpu().numpy()
+        r_rel = rel(got, o["recon"], A)
+        bit = bool(np.array_equal(got, owns[rcv]))
+        good = torch.tensor([1 if (r_rel <= 1e-4 and bit) else 0], device=dev)
+        dist.all_reduce(good, op=dist.ReduceOp.MIN)
+        report("pp_ring_sendrecv", recon_rel=r_rel, bitwise_equal_to_sender=bit, ok=bool(good.item()))
+
     # ------------------------------------------------------------------ EMB dense (fused, reading C12)
     V, h = 4096, 1024
     D = max(1, world // 2)

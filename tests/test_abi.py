@@ -31,7 +31,7 @@ def declared_functions():
 def test_header_declares_the_boundary():
     names = declared_functions()
     for want in ["occ_compress", "occ_decompress", "occ_allreduce_factors", "occ_send_factors",
-                 "occ_recv_factors", "occ_embed_sync", "occ_init_q", "occ_workspace_bytes",
+                 "occ_recv_factors", "occ_sendrecv_factors", "occ_embed_sync", "occ_init_q", "occ_workspace_bytes",
                  "occ_comm_init", "occ_comm_split", "occ_comm_destroy", "occ_get_unique_id"]:
         assert want in names
 
@@ -163,6 +163,8 @@ def test_allreduce_factors_rank_mismatch(L):
 def test_comm_null_handles(L):
     M, E, Q, P = good()
     s = L.occ_send_factors(M, E, Q, P, 16, 1, 0, None, ctypes.c_void_p(FAKE), 1 << 30, None)
+    assert status_name(L, s) == "OCC_ERR_INVALID_ARG"
+    s = L.occ_sendrecv_factors(M, E, Q, P, 16, 1, M, P, Q, 1, 0, None, ctypes.c_void_p(FAKE), 1 << 30, None)
     assert status_name(L, s) == "OCC_ERR_INVALID_ARG"
     assert L.occ_comm_destroy(None) == 0
 

@@ -191,6 +191,23 @@ def test_orient_t_matches_oracle(bf16, multi):
     check_step(g, o, M_used + e, tol=TOLBF if bf16 else TOL32)
 
 
+@pytest.mark.parametrize("bf16", [False, True])
+def test_decompress_bit_identical_to_sender_reconstruction(bf16):
+    """Reading C8: occ_decompress(P_hat, Q) on the receiver reproduces, bit for
+    bit, the M' the sender's e_new was taken against (same device arithmetic)."""
+    n, m, r = 1000, 1208, 16
+    M = synth.d2_gradlike(n, m, 91)
+    e = synth.e0(n, m, 92, like=M)
+    Q0 = synth.q0(m, r, 93)
+    g = run_gpu(M, e, Q0, r, bf16=bf16)
+    assert g["stats"]["path"] == 3
+    Pd, Qd = to_dev(g["P_hat"]), to_dev(g["Q"])
+    out = torch.empty(n, m, device="cuda", dtype=torch.bfloat16 if bf16 else torch.float32)
+    occ.occ_decompress(Pd, Qd, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.double().cpu().numpy(), g["recon"])
+
+
 def test_zero_input_all_fallbacks():
     n, m, r = 300, 264, 8
     M = np.zeros((n, m), np.float32)
