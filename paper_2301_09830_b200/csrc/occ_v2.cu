@@ -229,33 +229,31 @@ __device__ __noinline__ unsigned cold_orth_q(const Params2& p, Tile T, OrthW& o,
 // against (reading C8).  Work item = one warp x one 16-column group x 8 row
 // blocks; the Q fragment is loaded once per item.
 template <int R, bool BF>
-__global__ void __launch_bounds__(256) occ_v2_decompress_kernel(const float* __restrict__ P, const float* __restrict__ Q,
-                                                                void* __restrict__ out, long long ldo, int n, int m) {
+__global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const float* __restrict__ P,
+                                                                   const float* __restrict__ Q, void* __restrict__ out,
+                                                                   long long ldo, int n, int m) {
   constexpr int KS5 = K<R>::KS5, RBI = 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int ncg = (m + 15) / 16, nrb = (n + 7) / 8;
   const int nitems = ncg * ((nrb + RBI - 1) / RBI);
-  for (int item = blockIdx.x * 8 + warp; item < nitems; item += gridDim.x * 8) {
-    const int cg = item % ncg, rb0 = (item / ncg) * RBI;
-    unsigned qh[KS5][4], ql[KS5][4];
-    {  // A operand Q (M = columns 2g | 2g+1, K = rank), as in phase 5
-      const int cl = 16 * cg + 2 * g;
-      const bool okA = cl < m, okB = cl + 1 < m;
-      const float* qa_ = Q + (size_t)cl * R;
+  // operands of one work item (a 16-column group x RBI row blocks), fetched one
+  // item ahead so the L2 latency overlaps the previous item's MMAs and stores
+  auto fetch = [&](int item, float (&qv)[KS5][4], float (&pf)[RBI][KS5][2]) {
+    const bool ok = item < nitems;
+    const int cg = ok ? item % ncg : 0, rb0 = ok ? (item / ncg) * RBI : nrb;
+    const int cl = 16 * cg + 2 * g;   // A operand Q (M = columns 2g | 2g+1, K = rank), as in phase 5
+    const bool okA = ok && cl < m, okB = ok && cl + 1 < m;
+    const float* qa_ = Q + (size_t)cl * R;
 #pragma unroll
-      for (int ks = 0; ks < KS5; ks++) {
-        const int k0 = 8 * ks + t;
-        split3((okA && k0 < R) ? __ldg(qa_ + k0) : 0.f, qh[ks][0], ql[ks][0]);
-        split3((okB && k0 < R) ? __ldg(qa_ + R + k0) : 0.f, qh[ks][1], ql[ks][1]);
-        split3((okA && k0 + 4 < R) ? __ldg(qa_ + k0 + 4) : 0.f, qh[ks][2], ql[ks][2]);
-        split3((okB && k0 + 4 < R) ? __ldg(qa_ + R + k0 + 4) : 0.f, qh[ks][3], ql[ks][3]);
-      }
+    for (int ks = 0; ks < KS5; ks++) {
+      const int k0 = 8 * ks + t;
+      qv[ks][0] = (okA && k0 < R) ? __ldg(qa_ + k0) : 0.f;
+      qv[ks][1] = (okB && k0 < R) ? __ldg(qa_ + R + k0) : 0.f;
+      qv[ks][2] = (okA && k0 + 4 < R) ? __ldg(qa_ + k0 + 4) : 0.f;
+      qv[ks][3] = (okB && k0 + 4 < R) ? __ldg(qa_ + R + k0 + 4) : 0.f;
     }
-    // the B operand (P_hat^T, N = rows n/2 + 4(n&1)) of all RBI row blocks, loaded
-    // up front so the L2 latency is paid once per item, not once per row block
-    float pf[RBI][KS5][2];
 #pragma unroll
-    for (int j = 0; j < RBI; j++) {
+    for (int j = 0; j < RBI; j++) {   // B operand P_hat^T, N = rows n/2 + 4(n&1)
       const int rn = 8 * (rb0 + j) + (g >> 1) + 4 * (g & 1);
 #pragma unroll
       for (int ks = 0; ks < KS5; ks++) {
@@ -264,26 +262,43 @@ __global__ void __launch_bounds__(256) occ_v2_decompress_kernel(const float* __r
         pf[j][ks][1] = (rn < n && k + 4 < R) ? __ldg(P + (size_t)rn * R + k + 4) : 0.f;
       }
     }
+  };
+  const int stride = gridDim.x * 8;
+  int item = blockIdx.x * 8 + warp;
+  float qv[KS5][4], pf[RBI][KS5][2];
+  fetch(item, qv, pf);
+  for (; item < nitems; item += stride) {
+    const int cg = item % ncg, rb0 = (item / ncg) * RBI;
+    unsigned qh[KS5][4], ql[KS5][4];
+#pragma unroll
+    for (int ks = 0; ks < KS5; ks++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) split3(qv[ks][q], qh[ks][q], ql[ks][q]);
+    float mrs[RBI][4];
 #pragma unroll
     for (int j = 0; j < RBI; j++) {
-      const int rblk = rb0 + j;
-      if (rblk >= nrb) break;
-      float mr[4] = {0.f, 0.f, 0.f, 0.f};
+      mrs[j][0] = mrs[j][1] = mrs[j][2] = mrs[j][3] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < KS5; ks++) {
         unsigned h0, l0, h1, l1;
         split3(pf[j][ks][0], h0, l0);
         split3(pf[j][ks][1], h1, l1);
-        mma3(mr, qh[ks], ql[ks], h0, h1, l0, l1);
+        mma3(mrs[j], qh[ks], ql[ks], h0, h1, l0, l1);
       }
+    }
+    fetch(item + stride, qv, pf);   // next item's operands, in flight during the stores
+#pragma unroll
+    for (int j = 0; j < RBI; j++) {
+      const int rblk = rb0 + j;
+      if (rblk >= nrb) break;
       // mr: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
       const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
-      const int rows[2] = {r, r + 4};
 #pragma unroll
       for (int h = 0; h < 2; h++) {
-        if (rows[h] >= n || c >= m) continue;
-        const size_t o0 = (size_t)rows[h] * ldo + c;
-        const float v0 = mr[h], v1 = mr[2 + h];
+        const int row = r + 4 * h;
+        if (row >= n || c >= m) continue;
+        const size_t o0 = (size_t)row * ldo + c;
+        const float v0 = mrs[j][h], v1 = mrs[j][2 + h];
         if (BF) {
           __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(out) + o0;
           if (c + 1 < m) *reinterpret_cast<__nv_bfloat162*>(d) = __floats2bfloat162_rn(v0, v1);
@@ -499,7 +514,7 @@ size_t v2_tail_bytes(int64_t n, int64_t m, int r, int sms) {
 cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r, bool bf16,
                               cudaStream_t st) {
   const int items = ((m + 15) / 16) * (((n + 7) / 8 + 7) / 8);
-  const int grid = std::max(1, std::min((items + 7) / 8, 148 * 8));
+  const int grid = std::max(1, std::min((items + 7) / 8, 148 * 2));   // persistent: 2 CTAs per SM
   switch (r) {
 #define V2D(RR)                                                                                            \
   case RR:                                                                                                 \
