@@ -208,6 +208,28 @@ def test_decompress_bit_identical_to_sender_reconstruction(bf16):
     assert np.array_equal(out.double().cpu().numpy(), g["recon"])
 
 
+# BASELINE.json configs at full size, in the launch configuration bench.py times
+# (the fused kernel for r <= 32, the per-phase path for r = 64), elementwise
+# against the oracle (reading C6 matricisation; D2 gradient-like inputs).
+FULL = [
+    (4096, 1920, 16, 3),    # configs[1]: GPT-2.5B inter-stage, mb 4 (the bench line); fused kernel
+    (8192, 3072, 32, 1),    # configs[2] shape: GPT-8.3B inter-stage, mb 8; v1 fused kernel (the v2 tile plan does not fit)
+    (3072, 12288, 64, 1),   # configs[3] MLP weight gradient, r = 64: per-phase kernels
+]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n,m,r,path", FULL)
+def test_full_size_configs_match_oracle(n, m, r, path):
+    M = synth.d2_gradlike(n, m, 1000 + n)
+    e = synth.e0(n, m, 1001 + n, like=M)
+    Q0 = synth.q0(m, r, 1002)
+    g = run_gpu(M, e, Q0, r)
+    assert g["stats"]["path"] == path
+    o = oracle.compress_step(M, e, Q0)
+    check_step(g, o, M.astype(np.float64) + e, tol=TOL32, check_factors=False)
+
+
 def test_zero_input_all_fallbacks():
     n, m, r = 300, 264, 8
     M = np.zeros((n, m), np.float32)
