@@ -14,7 +14,7 @@ template <int R>
 __host__ __device__ constexpr size_t orth_bytes() { return (sizeof(OrthSmem<R>) + 15) / 16 * 16; }
 
 template <int R, bool DPL>
-__global__ void __launch_bounds__(NT) occ_step_kernel(Params p, int ph0, int ph1, int coop) {
+__global__ void __launch_bounds__(NT, (R <= 32) ? 2 : 1) occ_step_kernel(Params p, int ph0, int ph1, int coop) {
   extern __shared__ __align__(16) unsigned char smraw[];
   float* sm = reinterpret_cast<float*>(smraw);
   unsigned nb = 0;
