@@ -173,6 +173,9 @@ occ_status occ_embed_sync(occ_mat G, occ_mat err, occ_mat Q, occ_mat P, int r, f
 occ_status occ_get_unique_id(uint8_t id[128]);
 occ_status occ_comm_init(occ_comm* comm, const uint8_t id[128], int nranks, int rank);
 occ_status occ_comm_split(occ_comm parent, int color, int key, occ_comm* out);
+/* Adopt an existing ncclComm_t (e.g. torch's ProcessGroupNCCL communicator);
+ * occ_comm_destroy then frees only the handle, never the caller's communicator. */
+occ_status occ_comm_wrap(occ_comm* comm, void* nccl_comm);
 occ_status occ_comm_rank(occ_comm comm, int* rank, int* nranks);
 occ_status occ_comm_destroy(occ_comm comm);
 

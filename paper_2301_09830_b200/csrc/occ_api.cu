@@ -18,6 +18,7 @@ using namespace occ;
 struct occ_comm_s {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  bool owned = true;   // false for occ_comm_wrap: the caller's communicator is not destroyed
 };
 
 namespace {
@@ -559,9 +560,21 @@ occ_status occ_comm_rank(occ_comm comm, int* rank, int* nranks) {
   return OCC_OK;
 }
 
+occ_status occ_comm_wrap(occ_comm* comm, void* nccl_comm) {
+  if (!comm || !nccl_comm) return fail(OCC_ERR_INVALID_ARG, "bad comm_wrap args");
+  occ_comm c = new occ_comm_s;
+  c->comm = static_cast<ncclComm_t>(nccl_comm);
+  c->owned = false;
+  ncclResult_t nr = ncclCommUserRank(c->comm, &c->rank);
+  if (nr == ncclSuccess) nr = ncclCommCount(c->comm, &c->nranks);
+  if (nr != ncclSuccess) { delete c; return nccl_fail(nr, "occ_comm_wrap"); }
+  *comm = c;
+  return OCC_OK;
+}
+
 occ_status occ_comm_destroy(occ_comm comm) {
   if (!comm) return OCC_OK;
-  ncclResult_t nr = ncclCommDestroy(comm->comm);
+  ncclResult_t nr = comm->owned ? ncclCommDestroy(comm->comm) : ncclSuccess;
   delete comm;
   return nr == ncclSuccess ? OCC_OK : nccl_fail(nr, "ncclCommDestroy");
 }

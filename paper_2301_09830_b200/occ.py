@@ -78,6 +78,7 @@ def lib():
         "occ_get_unique_id": ([ctypes.c_char_p], c_int),
         "occ_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, c_int, c_int], c_int),
         "occ_comm_split": ([vp, c_int, c_int, ctypes.POINTER(vp)], c_int),
+        "occ_comm_wrap": ([ctypes.POINTER(vp), vp], c_int),
         "occ_comm_rank": ([vp, ctypes.POINTER(c_int), ctypes.POINTER(c_int)], c_int),
         "occ_comm_destroy": ([vp], c_int),
         "occ_check_status": ([vp, vp], c_int),
@@ -244,6 +245,14 @@ class Comm:
         dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
         h = ctypes.c_void_p()
         _check(lib().occ_comm_init(ctypes.byref(h), obj[0], world, rank), "occ_comm_init")
+        return cls(h.value)
+
+    @classmethod
+    def wrap(cls, nccl_comm_ptr: int) -> "Comm":
+        """Adopt an existing ncclComm_t (not destroyed by destroy()), e.g. the
+        communicator of a torch ProcessGroupNCCL (its private _comm_ptr())."""
+        h = ctypes.c_void_p()
+        _check(lib().occ_comm_wrap(ctypes.byref(h), ctypes.c_void_p(nccl_comm_ptr)), "occ_comm_wrap")
         return cls(h.value)
 
     def split(self, color: int, key: int) -> Optional["Comm"]:

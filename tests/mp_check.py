@@ -213,6 +213,30 @@ def main():
     e3 = rel(G.double().cpu().numpy(), o["recon"], A / D)
     report("emb_compressed_orient_t", recon_rel=e3, ok=e3 <= 1e-4)
 
+    # ------------------------------------------------------------------ occ_comm_wrap (torch's communicator)
+    try:
+        ptr = dist.distributed_c10d._get_default_group()._get_backend(dev)._comm_ptr()
+    except Exception as exc:   # private torch API: report, do not fail
+        ptr = None
+        report("comm_wrap", skipped=str(exc)[:80], ok=True)
+    if ptr:
+        wrapped = occ.Comm.wrap(ptr)
+        n, m, r = 512, 768, 8
+        Ms = [synth.d2_gradlike(n, m, 1300 + w) for w in range(world)]
+        Q0 = synth.q0(m, r, 19)
+        outs = []
+        for cm in (wrapped, comm):
+            G = torch.from_numpy(Ms[rank]).to(dev)
+            Q = torch.from_numpy(Q0).to(dev)
+            P = torch.empty(n, r, device=dev)
+            occ.occ_allreduce_factors([G], None, [Q], [P], r, 1.0 / world, flags=occ.OCC_NO_EF, comm=cm)
+            torch.cuda.synchronize()
+            outs.append(G.cpu())
+        same = bool(torch.equal(outs[0], outs[1]))
+        report("comm_wrap", nranks=wrapped.nranks, same_result_as_own_comm=same,
+               ok=same and wrapped.nranks == world and wrapped.rank == rank)
+        wrapped.destroy()   # frees only the handle
+
     comm.destroy()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)

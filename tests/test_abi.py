@@ -167,6 +167,8 @@ def test_comm_null_handles(L):
     s = L.occ_sendrecv_factors(M, E, Q, P, 16, 1, M, P, Q, 1, 0, None, ctypes.c_void_p(FAKE), 1 << 30, None)
     assert status_name(L, s) == "OCC_ERR_INVALID_ARG"
     assert L.occ_comm_destroy(None) == 0
+    h = ctypes.c_void_p()
+    assert status_name(L, L.occ_comm_wrap(ctypes.byref(h), None)) == "OCC_ERR_INVALID_ARG"
 
 
 def test_python_binding_fails_loudly_without_library(monkeypatch, tmp_path):
