@@ -82,7 +82,9 @@ typedef struct occ_comm_s* occ_comm; /* wraps an ncclComm_t */
 enum {
   OCC_NO_EF = 1u,          /* do not add err (Non-LEP / naive compression); err, if given, receives M - M' */
   OCC_EF_GLOBAL = 2u,      /* DP only: e_w = A_w - M' instead of the local A_w - P_hat Q_w^T (reading C2) */
-  OCC_CHECK_FINITE = 4u,   /* reserved: set a device status word on non-finite input (not yet implemented) */
+  OCC_CHECK_FINITE = 4u,   /* set a device status word when M or err holds a NaN / Inf (detected on the Gram
+                              diagonal, r checks per step; outputs still propagate it); occ_check_status
+                              reports OCC_ERR_NONFINITE and clears it */
   OCC_ORIENT_T = 16u,      /* compress A^T (reading C6, the 50257-row embedding): P is m x r (orthonormal,
                               column side), Q is n x r (row side, the warm start); M, err, recon keep their
                               stored n x m layout.  Runs on the per-phase kernels (not the fused one). */

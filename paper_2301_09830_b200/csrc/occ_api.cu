@@ -142,6 +142,7 @@ Params base_params(const occ_mat& M, const occ_mat& err, const occ_mat& Q, const
   p.tau = kTau;
   p.kappa_thr = kKappaTwoPass;
   p.force_two_pass = (flags & OCC_FORCE_TWO_PASS) ? 1 : 0;
+  p.check_finite = (flags & OCC_CHECK_FINITE) ? 1 : 0;
   return p;
 }
 
@@ -590,6 +591,8 @@ occ_status occ_check_status(cudaStream_t stream, occ_comm comm) {
     if (nr != ncclSuccess) return nccl_fail(nr, "ncclCommGetAsyncError");
     if (ar != ncclSuccess) return nccl_fail(ar, "nccl async");
   }
+  const unsigned nf = take_nonfinite_v1() | take_nonfinite_v2();
+  if (nf) return fail(OCC_ERR_NONFINITE, "non-finite M or err in a call made with OCC_CHECK_FINITE");
   return OCC_OK;
 }
 

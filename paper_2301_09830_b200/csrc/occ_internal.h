@@ -36,6 +36,9 @@ cudaError_t run_phases(const Params& p, const Geometry& g, int ph0, int ph1, boo
 cudaError_t run_decompress(const Params& p, int r, cudaStream_t st);
 size_t v2_tail_bytes(int64_t n, int64_t m, int r, int sms);
 cudaError_t run_v2(const Params& p, int r, void* ws_tail, size_t tail_avail, int sms, cudaStream_t st);
+// OCC_CHECK_FINITE: read and clear the device status words (occ_check_status)
+unsigned take_nonfinite_v1();
+unsigned take_nonfinite_v2();
 // out = round(P Q^T) with the fused kernel's phase-5 arithmetic (bit-identical
 // to the sender's reconstruction, reading C8); cudaErrorNotSupported if r > 32.
 cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r, bool bf16,

@@ -81,6 +81,7 @@ struct Params {
   double tau;
   double kappa_thr;
   int force_two_pass;
+  int check_finite;      // OCC_CHECK_FINITE: flag a non-finite Gram diagonal (non-finite M or e)
   int path;
 };
 
@@ -468,12 +469,19 @@ __device__ void gram_partial(const float* src, int r0, int nr, double* part_u, f
 }
 
 // C.1: Cholesky-detect.  Returns plan: 0 done, 2 slow path needed (deg), 3 second pass needed.
+// OCC_CHECK_FINITE status word of the v1 kernels (read and cleared by
+// occ_check_status; one per device context).  A NaN or Inf anywhere in M or e
+// reaches P = (M + e) Q and so the Gram diagonal: r checks per step.
+__device__ unsigned g_nonfinite_v1 = 0;
+
 template <int R>
 __device__ int phase_C1(const Params& p, OrthSmem<R>& o, float* ps) {
   const int units = (p.n + B_ROWS - 1) / B_ROWS;
   const double tau2 = p.tau * p.tau;
   reduce_gram<R>(p.G_part, p.ngp, o.S);
   __syncthreads();
+  if (p.check_finite && blockIdx.x == 0 && threadIdx.x < R && !isfinite(o.S[threadIdx.x * R + threadIdx.x]))
+    atomicOr(&g_nonfinite_v1, 1u);
   const int deg = chol_inplace<R>(o.S, o.gdiag, tau2, true, &o.flag);
   if (deg) {
     // X = P^T F, Y = F^T F partials for this CTA's rows

@@ -244,6 +244,14 @@ cudaError_t run_decompress(const Params& p, int r, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+// OCC_CHECK_FINITE: read and clear this device's v1 status word.
+unsigned take_nonfinite_v1() {
+  unsigned v = 0, z = 0;
+  if (cudaMemcpyFromSymbol(&v, g_nonfinite_v1, sizeof v) != cudaSuccess) return 0;
+  if (v) cudaMemcpyToSymbol(g_nonfinite_v1, &z, sizeof z);
+  return v;
+}
+
 // ------------------------------------------------------------------ init_q
 __global__ void occ_init_q_kernel(float* q, long long rows, int r, long long ld, unsigned long long seed) {
   const long long total = rows * r;

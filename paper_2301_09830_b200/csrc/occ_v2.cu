@@ -17,6 +17,9 @@ static_assert(2 * occ::v2::kTrStamps == occ::kTraceSlots, "trace layout");
 namespace occ {
 namespace v2 {
 
+// OCC_CHECK_FINITE status word of the fused kernel (see g_nonfinite_v1).
+__device__ unsigned g_nonfinite_v2 = 0;
+
 // ------------------------------------------------------------------ cold paths
 // Out of line (see the kernel's phase 3): taken only when a column is
 // degenerate (reading C3) or the first pass is ill conditioned (reading C5).
@@ -463,6 +466,7 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
   // general path.
   p.amp_thr = (p.debug & 4) ? -1.0 : 32.0;
   p.spec = (pl.cells_per_warp <= TMEM_CELLS && !(p.debug & 16)) ? 1 : 0;
+  p.check_finite = p1.check_finite;
   auto kern = occ_v2_kernel<R, MBF>;
   // the dynamic-SMEM opt-in only ever grows; set it when a plan needs more
   // (per device: the attribute is per-context state)
@@ -509,6 +513,13 @@ size_t v2_tail_bytes(int64_t n, int64_t m, int r, int sms) {
 #undef V2T
   }
   return 0;
+}
+
+unsigned take_nonfinite_v2() {
+  unsigned v = 0, z = 0;
+  if (cudaMemcpyFromSymbol(&v, v2::g_nonfinite_v2, sizeof v) != cudaSuccess) return 0;
+  if (v) cudaMemcpyToSymbol(v2::g_nonfinite_v2, &z, sizeof z);
+  return v;
 }
 
 cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r, bool bf16,

@@ -75,6 +75,7 @@ struct Params2 {
   unsigned long long fb_seed;
   double tau, kappa_thr;
   double amp_thr;      // fused-Q gate on ||S Li^T||_F (phase 3)
+  int check_finite;    // OCC_CHECK_FINITE (phase 3)
   int spec;            // every cell TMEM-resident: the fused result is checked after phase 5
   int force_two_pass;
   int debug;           // bit 0: skip phase-1 compute (streaming floor measurement only)

@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   bool deg;
   if (w == NW - 1) {
     asm volatile("bar.sync 3, %0;" ::"r"((NWA + 1) * 32) : "memory");
+    if (p.check_finite && blockIdx.x == 0 && lane < R && !isfinite(o.gdiag[lane])) atomicOr(&g_nonfinite_v2, 1u);
     deg = ldl_warp_unrolled<R>(o, p.tau * p.tau, true) != 0;
     trw(8);
     if (!deg) {

@@ -230,6 +230,32 @@ def test_full_size_configs_match_oracle(n, m, r, path):
     check_step(g, o, M.astype(np.float64) + e, tol=TOL32, check_factors=False)
 
 
+@pytest.mark.parametrize("v1", [False, True])
+def test_check_finite_reports_nonfinite_input(monkeypatch, v1):
+    """OCC_CHECK_FINITE: a NaN in M (or err) sets the device status word that
+    occ_check_status reports (and clears); clean input and calls without the
+    flag report nothing."""
+    if v1:
+        monkeypatch.setenv("OCC_PATH", "v1")
+    n, m, r = 300, 264, 8
+    M = synth.d2_gradlike(n, m, 95)
+    e = synth.e0(n, m, 96, like=M)
+    Q0 = synth.q0(m, r, 97)
+    occ.occ_check_status()                                    # clear anything pending
+    run_gpu(M, e, Q0, r, flags=occ.OCC_CHECK_FINITE)
+    occ.occ_check_status()                                    # clean: no error
+    Mn = M.copy()
+    Mn[17, 23] = np.nan
+    run_gpu(Mn, e, Q0, r)                                     # no flag: nothing recorded
+    occ.occ_check_status()
+    g = run_gpu(Mn, e, Q0, r, flags=occ.OCC_CHECK_FINITE)
+    assert g["stats"]["path"] == (1 if v1 else 3)
+    with pytest.raises(occ.OccError) as exc:
+        occ.occ_check_status()
+    assert exc.value.name == "OCC_ERR_NONFINITE"
+    occ.occ_check_status()                                    # cleared by the report
+
+
 def test_zero_input_all_fallbacks():
     n, m, r = 300, 264, 8
     M = np.zeros((n, m), np.float32)
