@@ -85,6 +85,9 @@ enum {
   OCC_CHECK_FINITE = 4u,   /* set a device status word when M or err holds a NaN / Inf (detected on the Gram
                               diagonal, r checks per step; outputs still propagate it); occ_check_status
                               reports OCC_ERR_NONFINITE and clears it */
+  OCC_WIRE_BF16 = 8u,      /* reading C7: P_hat and Q are rounded to bf16 before the reconstruction (so e_new
+                              and the returned factors use the rounded values) and sent as bf16 by the
+                              send / recv calls (half the bytes).  Not for occ_allreduce_factors. */
   OCC_ORIENT_T = 16u,      /* compress A^T (reading C6, the 50257-row embedding): P is m x r (orthonormal,
                               column side), Q is n x r (row side, the warm start); M, err, recon keep their
                               stored n x m layout.  Runs on the per-phase kernels (not the fused one). */

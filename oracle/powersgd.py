@@ -129,7 +129,8 @@ def round_to(x: np.ndarray, out_dtype: str) -> np.ndarray:
 # --------------------------------------------------------------------------
 
 def compress_step(M, e_old, Q_prev, *, out_dtype: str = "f64", tau: float = 1e-5,
-                  fb_seed: int = 0, no_ef: bool = False, orient_t: bool = False):
+                  fb_seed: int = 0, no_ef: bool = False, orient_t: bool = False,
+                  wire_bf16: bool = False):
     """One warm-started power-iteration step with error feedback.
 
     A      = M + e_old                 (a1; Non-LEP / NO_EF: e_old treated as 0)
@@ -141,6 +142,9 @@ def compress_step(M, e_old, Q_prev, *, out_dtype: str = "f64", tau: float = 1e-5
 
     orient_t (reading C6, used for the 50257-row embedding): compress A^T
     instead of A; M' and e_new are returned in A's stored layout.
+    wire_bf16 (reading C7, OCC_WIRE_BF16): the factors are computed as above
+    and then rounded to bf16 (RNE) for the wire; M' and e_new are taken
+    against the rounded factors, which are also the returned P_hat and Q.
     Returns a dict with P_hat, Q, recon (M'), err (e_new), fallbacks.
     """
     M = np.asarray(M, dtype=np.float64)
@@ -150,6 +154,8 @@ def compress_step(M, e_old, Q_prev, *, out_dtype: str = "f64", tau: float = 1e-5
     P = X @ Q_prev
     P_hat, fb = mgs2(P, tau, fb_seed)
     Q = X.T @ P_hat
+    if wire_bf16:
+        P_hat, Q = round_to(P_hat, "bf16"), round_to(Q, "bf16")
     R = round_to(P_hat @ Q.T, out_dtype)
     if orient_t:
         R = R.T

@@ -143,6 +143,7 @@ Params base_params(const occ_mat& M, const occ_mat& err, const occ_mat& Q, const
   p.kappa_thr = kKappaTwoPass;
   p.force_two_pass = (flags & OCC_FORCE_TWO_PASS) ? 1 : 0;
   p.check_finite = (flags & OCC_CHECK_FINITE) ? 1 : 0;
+  p.wire_bf16 = (flags & OCC_WIRE_BF16) ? 1 : 0;
   return p;
 }
 
@@ -165,6 +166,18 @@ occ_status nccl_fail(ncclResult_t r, const char* what) {
 // [2,6) = Gram + orthonormalisation, [6,8) = sweep 2 + Q reduce, [8,9) = reconstruct.
 constexpr int kPhA = 0, kPhOrth = 2, kPhD = 6, kPhF = 8, kPhEnd = 9;
 
+// phase F of a per-phase occ_compress (M' and e_new): the v2 decompress
+// arithmetic, so occ_decompress reproduces the sender's M' bit for bit (C8)
+// whichever path compressed; v1 phase F for r = 64, which occ_decompress also
+// runs in v1 (and under OCC_PATH=v1, where both sides are v1).
+cudaError_t reconstruct(const Params& p, const Geometry& g, int r, bool multi, cudaStream_t st) {
+  if (!want_v1()) {
+    cudaError_t e = run_v2_reconstruct(p, r, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  return run_phases(p, g, kPhF, kPhEnd, multi, false, st);
+}
+
 // Orthonormalise the column-side factor U (m x R, in place) with the per-phase
 // kernels: the Gram phases run with the factor length m (OCC_ORIENT_T).
 cudaError_t orth_column_factor(const Params& base, float* U, int64_t m, int64_t n, int R, const WsLayout& L,
@@ -176,6 +189,43 @@ cudaError_t orth_column_factor(const Params& base, float* U, int64_t m, int64_t 
   Geometry gT = make_geometry(m, n, R, kGeomSms);
   fill_ws(p2, gT, L, ws);
   return run_phases(p2, gT, kPhOrth, kPhD, multi, false, st);
+}
+
+// OCC_WIRE_BF16 send side: the (already bf16-exact) factors packed into the
+// workspace's factor buckets, then sent as bf16.  Queues the ncclSends (inside
+// the caller's group).
+occ_status send_factors_bf16(const occ_mat& P, const occ_mat& Q, int r, int peer, occ_comm pp, void* ws,
+                             size_t ws_bytes, int64_t n, int64_t m, cudaStream_t st) {
+  const WsLayout L = make_layout(make_geometry(n, m, r, kGeomSms), 1);
+  const size_t need = 2 * ((size_t)P.rows + (size_t)Q.rows) * r;
+  if (L.qs_bucket - L.p_bucket < need || ws_bytes < L.total) return fail(OCC_ERR_WORKSPACE, "bf16 staging");
+  char* stage = static_cast<char*>(ws) + L.p_bucket;
+  cudaError_t e = run_pack_bf16(static_cast<const float*>(P.ptr), stage, (long long)P.rows * r, st);
+  if (e == cudaSuccess) e = run_pack_bf16(static_cast<const float*>(Q.ptr), stage + 2 * (size_t)P.rows * r, (long long)Q.rows * r, st);
+  if (e != cudaSuccess) return cuda_fail(e, "bf16 pack");
+  ncclSend(stage, (size_t)P.rows * r, ncclBfloat16, peer, pp->comm, st);
+  ncclSend(stage + 2 * (size_t)P.rows * r, (size_t)Q.rows * r, ncclBfloat16, peer, pp->comm, st);
+  return OCC_OK;
+}
+
+// OCC_WIRE_BF16 receive side: bf16 factors land in `out` (not yet written), are
+// expanded into Prcv / Qrcv, and `out` is then overwritten by the decompression.
+occ_status recv_factors_bf16(const occ_mat& out, const occ_mat& Prcv, const occ_mat& Qrcv, int r, int peer,
+                             occ_comm pp, cudaStream_t st) {
+  const size_t need = 2 * ((size_t)Prcv.rows + (size_t)Qrcv.rows) * r;
+  const size_t have = (size_t)out.rows * out.ld * (out.dtype == OCC_BF16 ? 2 : 4);
+  if (have < need) return fail(OCC_ERR_UNSUPPORTED, "OCC_WIRE_BF16: out too small to stage the factors");
+  char* stage = static_cast<char*>(out.ptr);
+  ncclRecv(stage, (size_t)Prcv.rows * r, ncclBfloat16, peer, pp->comm, st);
+  ncclRecv(stage + 2 * (size_t)Prcv.rows * r, (size_t)Qrcv.rows * r, ncclBfloat16, peer, pp->comm, st);
+  return OCC_OK;
+}
+occ_status unpack_factors_bf16(const occ_mat& out, const occ_mat& Prcv, const occ_mat& Qrcv, int r, cudaStream_t st) {
+  const char* stage = static_cast<const char*>(out.ptr);
+  cudaError_t e = run_unpack_bf16(stage, static_cast<float*>(Prcv.ptr), (long long)Prcv.rows * r, st);
+  if (e == cudaSuccess)
+    e = run_unpack_bf16(stage + 2 * (size_t)Prcv.rows * r, static_cast<float*>(Qrcv.ptr), (long long)Qrcv.rows * r, st);
+  return e == cudaSuccess ? OCC_OK : cuda_fail(e, "bf16 unpack");
 }
 
 }  // namespace
@@ -250,11 +300,13 @@ occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat re
       p3.P = Qp;
       e = run_phases(p3, g, kPhA, kPhOrth, multi, false, stream);
     }
+    if (e == cudaSuccess && p.wire_bf16) e = run_round_bf16(Pp, M.cols * (long long)r, stream);
+    if (e == cudaSuccess && p.wire_bf16) e = run_round_bf16(Qp, M.rows * (long long)r, stream);
     if (e == cudaSuccess) {
       Params p4 = p;
       p4.P = Qp;
       p4.Qrec = Pp;
-      e = run_phases(p4, g, kPhF, kPhEnd, multi, false, stream);
+      e = reconstruct(p4, g, r, multi, stream);
     }
     return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_compress (OCC_ORIENT_T) launch");
   }
@@ -263,7 +315,13 @@ occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat re
     if (e2 == cudaSuccess) return OCC_OK;
     if (e2 != cudaErrorNotSupported) return cuda_fail(e2, "occ_compress (fused v2) launch");
   }
-  cudaError_t e = run_phases(p, g, 0, 9, multi, false, stream);
+  cudaError_t e;
+  e = run_phases(p, g, kPhA, kPhF, multi, false, stream);
+  if (p.wire_bf16) {   // reading C7: the reconstruction uses the bf16-rounded factors
+    if (e == cudaSuccess) e = run_round_bf16(p.P, M.rows * (long long)r, stream);
+    if (e == cudaSuccess) e = run_round_bf16(p.Qloc, M.cols * (long long)r, stream);
+  }
+  if (e == cudaSuccess) e = reconstruct(p, g, r, multi, stream);
   return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_compress launch");
 }
 
@@ -298,6 +356,7 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
                                  cudaStream_t stream) {
   if (nmat < 1 || !G || !Q || !P || !r) return fail(OCC_ERR_INVALID_ARG, "null array or nmat < 1");
   if (!(flags & OCC_NO_EF) && !err) return fail(OCC_ERR_INVALID_ARG, "err array required unless OCC_NO_EF");
+  if (flags & OCC_WIRE_BF16) return fail(OCC_ERR_UNSUPPORTED, "OCC_WIRE_BF16 applies to the send / recv calls");
   const int R = r[0];
   int64_t nmax = 0, mmax = 0;
   for (int i = 0; i < nmat; i++) {
@@ -436,8 +495,13 @@ occ_status occ_send_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r,
   if (s) return s;
   ncclResult_t nr;
   if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
-  ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream);   // (OCC_ORIENT_T: P is m x r)
-  ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream);
+  if (flags & OCC_WIRE_BF16) {
+    s = send_factors_bf16(P, Q, r, peer, pp, ws, ws_bytes, M.rows, M.cols, stream);
+    if (s) { ncclGroupEnd(); return s; }
+  } else {
+    ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream);   // (OCC_ORIENT_T: P is m x r)
+    ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream);
+  }
   if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclSend(P,Q)");
   return OCC_OK;
 }
@@ -451,11 +515,18 @@ occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, 
   occ_status s = check_view(P, "P", ot ? out.cols : out.rows, r, true, true);
   if (s) return s;
   if ((s = check_view(Q, "Q", ot ? out.rows : out.cols, r, true, true))) return s;
+  const bool wire = (flags & OCC_WIRE_BF16) != 0;
   ncclResult_t nr;
   if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
-  ncclRecv(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream);
-  ncclRecv(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream);
+  if (wire) {
+    s = recv_factors_bf16(out, P, Q, r, peer, pp, stream);
+    if (s) { ncclGroupEnd(); return s; }
+  } else {
+    ncclRecv(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream);
+    ncclRecv(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream);
+  }
   if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclRecv(P,Q)");
+  if (wire && (s = unpack_factors_bf16(out, P, Q, r, stream))) return s;
   return ot ? occ_decompress(Q, P, out, stream) : occ_decompress(P, Q, out, stream);
 }
 
@@ -478,18 +549,33 @@ occ_status occ_sendrecv_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, in
     occ_status s = occ_compress(M, err, Q, P, none, r, flags, ws, ws_bytes, stream);
     if (s) return s;
   }
+  const bool wire = (flags & OCC_WIRE_BF16) != 0;
   ncclResult_t nr;
   if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
   if (snd) {
-    ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, send_peer, pp->comm, stream);
-    ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, send_peer, pp->comm, stream);
+    if (wire) {
+      occ_status s = send_factors_bf16(P, Q, r, send_peer, pp, ws, ws_bytes, M.rows, M.cols, stream);
+      if (s) { ncclGroupEnd(); return s; }
+    } else {
+      ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, send_peer, pp->comm, stream);
+      ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, send_peer, pp->comm, stream);
+    }
   }
   if (rcv) {
-    ncclRecv(Prcv.ptr, (size_t)Prcv.rows * r, ncclFloat, recv_peer, pp->comm, stream);
-    ncclRecv(Qrcv.ptr, (size_t)Qrcv.rows * r, ncclFloat, recv_peer, pp->comm, stream);
+    if (wire) {
+      occ_status s = recv_factors_bf16(out, Prcv, Qrcv, r, recv_peer, pp, stream);
+      if (s) { ncclGroupEnd(); return s; }
+    } else {
+      ncclRecv(Prcv.ptr, (size_t)Prcv.rows * r, ncclFloat, recv_peer, pp->comm, stream);
+      ncclRecv(Qrcv.ptr, (size_t)Qrcv.rows * r, ncclFloat, recv_peer, pp->comm, stream);
+    }
   }
   if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclSendRecv(P,Q)");
   if (!rcv) return OCC_OK;
+  if (wire) {
+    occ_status s = unpack_factors_bf16(out, Prcv, Qrcv, r, stream);
+    if (s) return s;
+  }
   return ot ? occ_decompress(Qrcv, Prcv, out, stream) : occ_decompress(Prcv, Qrcv, out, stream);
 }
 

@@ -82,6 +82,7 @@ struct Params {
   double kappa_thr;
   int force_two_pass;
   int check_finite;      // OCC_CHECK_FINITE: flag a non-finite Gram diagonal (non-finite M or e)
+  int wire_bf16;         // OCC_WIRE_BF16: round P_hat and Q to bf16 before the reconstruction
   int path;
 };
 

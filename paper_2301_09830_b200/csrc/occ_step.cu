@@ -72,7 +72,9 @@ __global__ void __launch_bounds__(NT, (R <= 32) ? 2 : 1) occ_step_kernel(Params 
       }
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && ph0 <= P_F && P_F < ph1) {
+  // stamped by the launch that ends the step's v1 part: phase F, or phase E when
+  // F runs in the v2 reconstruct kernel (occ_api.cu reconstruct)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ph0 <= P_F && P_E < ph1) {
     p.stats->path = p.path;
     p.stats->grid = gridDim.x;
     p.stats->q_amp = -1.0;
@@ -250,6 +252,33 @@ unsigned take_nonfinite_v1() {
   if (cudaMemcpyFromSymbol(&v, g_nonfinite_v1, sizeof v) != cudaSuccess) return 0;
   if (v) cudaMemcpyToSymbol(g_nonfinite_v1, &z, sizeof z);
   return v;
+}
+
+// ------------------------------------------------------------------ bf16 wire (OCC_WIRE_BF16)
+__global__ void occ_round_bf16_kernel(float* x, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+    x[i] = __bfloat162float(__float2bfloat16_rn(x[i]));
+}
+__global__ void occ_pack_bf16_kernel(const float* x, __nv_bfloat16* y, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+__global__ void occ_unpack_bf16_kernel(const __nv_bfloat16* y, float* x, long long count) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
+    x[i] = __bfloat162float(y[i]);
+}
+static int grid_for(long long count) { return (int)std::max<long long>(1, std::min<long long>((count + 255) / 256, 4096)); }
+cudaError_t run_round_bf16(float* x, long long count, cudaStream_t st) {
+  occ_round_bf16_kernel<<<grid_for(count), 256, 0, st>>>(x, count);
+  return cudaGetLastError();
+}
+cudaError_t run_pack_bf16(const float* x, void* y, long long count, cudaStream_t st) {
+  occ_pack_bf16_kernel<<<grid_for(count), 256, 0, st>>>(x, static_cast<__nv_bfloat16*>(y), count);
+  return cudaGetLastError();
+}
+cudaError_t run_unpack_bf16(const void* y, float* x, long long count, cudaStream_t st) {
+  occ_unpack_bf16_kernel<<<grid_for(count), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(y), x, count);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ init_q

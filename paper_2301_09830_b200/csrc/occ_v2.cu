@@ -231,10 +231,30 @@ __device__ __noinline__ unsigned cold_orth_q(const Params2& p, Tile T, OrthW& o,
 // receiver's M' is bit-identical to the M' the sender's e_new was taken
 // against (reading C8).  Work item = one warp x one 16-column group x 8 row
 // blocks; the Q fragment is loaded once per item.
-template <int R, bool BF>
-__global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const float* __restrict__ P,
-                                                                   const float* __restrict__ Q, void* __restrict__ out,
-                                                                   long long ldo, int n, int m) {
+// EF = true is the sender-side reconstruction of the per-phase paths
+// (occ_compress when the fused kernel does not take the shape, OCC_ORIENT_T):
+// the same M' plus e_new = (M + e_old) - M', so every sender's e_new is taken
+// against the M' occ_decompress reproduces (C8), whichever path compressed.
+struct DecArgs {
+  const float* P;            // n x R, row side
+  const float* Q;            // m x R, column side
+  void* out;                 // n x m (ldo), fp32 or bf16 (BF); nullptr: not written (EF only)
+  long long ldo;
+  int n, m;
+  const void* M;             // EF: n x m (ldm), fp32 or bf16 (m_bf16)
+  long long ldm;
+  int m_bf16;
+  const float* err_in;       // EF: e_old (lde_in) or nullptr (OCC_NO_EF)
+  long long lde_in;
+  float* err_out;            // EF: e_new (lde_out); may equal err_in
+  long long lde_out;
+};
+
+template <int R, bool BF, bool EF>
+__global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs d) {
+  const float* __restrict__ P = d.P;
+  const float* __restrict__ Q = d.Q;
+  const int n = d.n, m = d.m;
   constexpr int KS5 = K<R>::KS5, RBI = 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int ncg = (m + 15) / 16, nrb = (n + 7) / 8;
@@ -300,16 +320,55 @@ __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const float* 
       for (int h = 0; h < 2; h++) {
         const int row = r + 4 * h;
         if (row >= n || c >= m) continue;
-        const size_t o0 = (size_t)row * ldo + c;
-        const float v0 = mrs[j][h], v1 = mrs[j][2 + h];
-        if (BF) {
-          __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(out) + o0;
-          if (c + 1 < m) *reinterpret_cast<__nv_bfloat162*>(d) = __floats2bfloat162_rn(v0, v1);
-          else d[0] = __float2bfloat16_rn(v0);
-        } else {
-          float* d = reinterpret_cast<float*>(out) + o0;
-          if (c + 1 < m) *reinterpret_cast<float2*>(d) = make_float2(v0, v1);
-          else d[0] = v0;
+        const bool two = c + 1 < m;
+        float v0 = mrs[j][h], v1 = mrs[j][2 + h];
+        if (BF) {   // M' as the receiver decodes it (bf16), also what e_new is taken against
+          v0 = __bfloat162float(__float2bfloat16_rn(v0));
+          v1 = __bfloat162float(__float2bfloat16_rn(v1));
+        }
+        if (d.out) {
+          const size_t o0 = (size_t)row * d.ldo + c;
+          if (BF) {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(d.out) + o0;
+            if (two) *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
+            else dst[0] = __float2bfloat16_rn(v0);
+          } else {
+            float* dst = reinterpret_cast<float*>(d.out) + o0;
+            if (two) *reinterpret_cast<float2*>(dst) = make_float2(v0, v1);
+            else dst[0] = v0;
+          }
+        }
+        if constexpr (EF) {
+          float a0, a1 = 0.f;
+          if (d.m_bf16) {
+            const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(d.M) + (size_t)row * d.ldm + c;
+            if (two) {
+              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(src));
+              a0 = f.x; a1 = f.y;
+            } else {
+              a0 = __bfloat162float(src[0]);
+            }
+          } else {
+            const float* src = reinterpret_cast<const float*>(d.M) + (size_t)row * d.ldm + c;
+            if (two) {
+              const float2 f = __ldcs(reinterpret_cast<const float2*>(src));
+              a0 = f.x; a1 = f.y;
+            } else {
+              a0 = src[0];
+            }
+          }
+          if (d.err_in) {
+            const float* src = d.err_in + (size_t)row * d.lde_in + c;
+            if (two) {
+              const float2 f = *reinterpret_cast<const float2*>(src);
+              a0 += f.x; a1 += f.y;
+            } else {
+              a0 += src[0];
+            }
+          }
+          float* dst = d.err_out + (size_t)row * d.lde_out + c;
+          if (two) *reinterpret_cast<float2*>(dst) = make_float2(a0 - v0, a1 - v1);
+          else dst[0] = a0 - v0;
         }
       }
     }
@@ -467,6 +526,7 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
   p.amp_thr = (p.debug & 4) ? -1.0 : 32.0;
   p.spec = (pl.cells_per_warp <= TMEM_CELLS && !(p.debug & 16)) ? 1 : 0;
   p.check_finite = p1.check_finite;
+  p.wire_bf16 = p1.wire_bf16;
   auto kern = occ_v2_kernel<R, MBF>;
   // the dynamic-SMEM opt-in only ever grows; set it when a plan needs more
   // (per device: the attribute is per-context state)
@@ -522,20 +582,40 @@ unsigned take_nonfinite_v2() {
   return v;
 }
 
-cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r, bool bf16,
-                              cudaStream_t st) {
-  const int items = ((m + 15) / 16) * (((n + 7) / 8 + 7) / 8);
+static cudaError_t launch_v2_decompress(const v2::DecArgs& d, int r, bool bf16, bool ef, cudaStream_t st) {
+  const int items = ((d.m + 15) / 16) * (((d.n + 7) / 8 + 7) / 8);
   const int grid = std::max(1, std::min((items + 7) / 8, 148 * 2));   // persistent: 2 CTAs per SM
   switch (r) {
-#define V2D(RR)                                                                                            \
-  case RR:                                                                                                 \
-    if (bf16) v2::occ_v2_decompress_kernel<RR, true><<<grid, 256, 0, st>>>(P, Q, out, ldo, n, m);          \
-    else v2::occ_v2_decompress_kernel<RR, false><<<grid, 256, 0, st>>>(P, Q, out, ldo, n, m);              \
+#define V2D(RR)                                                                                     \
+  case RR:                                                                                          \
+    if (ef) {                                                                                       \
+      if (bf16) v2::occ_v2_decompress_kernel<RR, true, true><<<grid, 256, 0, st>>>(d);              \
+      else v2::occ_v2_decompress_kernel<RR, false, true><<<grid, 256, 0, st>>>(d);                 \
+    } else {                                                                                        \
+      if (bf16) v2::occ_v2_decompress_kernel<RR, true, false><<<grid, 256, 0, st>>>(d);             \
+      else v2::occ_v2_decompress_kernel<RR, false, false><<<grid, 256, 0, st>>>(d);                \
+    }                                                                                               \
     return cudaGetLastError();
     V2D(4) V2D(8) V2D(16) V2D(32)
 #undef V2D
   }
   return cudaErrorNotSupported;
+}
+
+cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r, bool bf16,
+                              cudaStream_t st) {
+  v2::DecArgs d{};
+  d.P = P; d.Q = Q; d.out = out; d.ldo = ldo; d.n = n; d.m = m;
+  return launch_v2_decompress(d, r, bf16, false, st);
+}
+
+cudaError_t run_v2_reconstruct(const Params& p, int r, cudaStream_t st) {
+  if (!p.err_out) return run_v2_decompress(p.P, p.Qrec, p.recon, p.ldr, p.n, p.m, r, p.r_bf16 != 0, st);
+  v2::DecArgs d{};
+  d.P = p.P; d.Q = p.Qrec; d.out = p.recon; d.ldo = p.ldr; d.n = p.n; d.m = p.m;
+  d.M = p.M; d.ldm = p.ldm; d.m_bf16 = p.m_bf16;
+  d.err_in = p.err_in; d.lde_in = p.lde_in; d.err_out = p.err_out; d.lde_out = p.lde_out;
+  return launch_v2_decompress(d, r, p.r_bf16 != 0, true, st);
 }
 
 cudaError_t run_v2(const Params& p, int r, void* ws_tail, size_t tail_avail, int sms, cudaStream_t st) {

@@ -76,6 +76,7 @@ struct Params2 {
   double tau, kappa_thr;
   double amp_thr;      // fused-Q gate on ||S Li^T||_F (phase 3)
   int check_finite;    // OCC_CHECK_FINITE (phase 3)
+  int wire_bf16;       // OCC_WIRE_BF16: P_hat rows and the Q slice rounded to bf16 before phase 5
   int spec;            // every cell TMEM-resident: the fused result is checked after phase 5
   int force_two_pass;
   int debug;           // bit 0: skip phase-1 compute (streaming floor measurement only)

@@ -383,6 +383,16 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
     nb = cold_orth_q<R, MBF>(p, T, o, ps, ps2, gscr, pa, taddr_w, nb, active, deg);
     phat = ps;
   }
+  if (p.wire_bf16 && w < NCW && active) {
+    // OCC_WIRE_BF16 (reading C7): the factors that leave the GPU are bf16, so
+    // the reconstruction and e_new use the rounded values (this CTA's P_hat
+    // rows and the Q slice it wrote; the slices are read by others after B3)
+    SyncCompute()();
+    auto rb = [](float x) { return __bfloat162float(__float2bfloat16_rn(x)); };
+    for (int x = tid; x < H8 * R; x += NCW * 32) phat[(x / R) * RP + x % R] = rb(phat[(x / R) * RP + x % R]);
+    float* qs_out = p.Qout + (size_t)(T.col0 + qs_cols.x) * R;
+    for (int x = tid; x < nqc * R; x += NCW * 32) qs_out[x] = rb(qs_out[x]);
+  }
   tr(12);
   for (int pass = 0;; pass++) {
     if (w < NCW) {

@@ -19,6 +19,7 @@ OCC_F32, OCC_BF16 = 0, 1
 OCC_NO_EF = 1
 OCC_EF_GLOBAL = 2
 OCC_CHECK_FINITE = 4
+OCC_WIRE_BF16 = 8
 OCC_ORIENT_T = 16
 OCC_FORCE_MULTI = 64
 OCC_FORCE_TWO_PASS = 128

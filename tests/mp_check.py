@@ -4,8 +4,9 @@
 
 Checks, against the fp64 oracle simulating all ranks in-process:
   * DP   occ_allreduce_factors over all ranks (local and global EF, reading C1/C2)
-  * PP   occ_send_factors (rank 1) -> occ_recv_factors (rank 0); the receiver's M'
-         must equal the sender's own decompression bit for bit (reading C8)
+  * PP   occ_send_factors (rank 1) -> occ_recv_factors (rank 0) and the sendrecv ring;
+         the receiver's M' must equal the sender's own decompression bit for bit
+         (reading C8); fp32 and bf16 (OCC_WIRE_BF16, C7) wire factors
   * EMB  occ_embed_sync dense (r = 0, reading C12) and compressed (r > 0, C14)
 Prints one JSON line per check on rank 0 and exits non-zero on any failure.
 """
@@ -100,79 +101,83 @@ def main():
         report(name, recon_rel=e_recon, err_rel=e_err, q_rel=q_rel, orth=orth, identical_on_ranks=same,
                ok=e_recon <= 1e-4 and e_err <= 1e-4 and same and orth <= 1e-5 and q_rel <= 1e-3)
 
-    # ------------------------------------------------------------------ PP (pairs 1 -> 0, 3 -> 2, ...)
-    if world >= 2:
-        n, m, r = 2048, 3072, 32      # BASELINE configs[2] shape class (8.3B hidden), shortened rows
-        sender = rank % 2 == 1
-        peer = rank - 1 if sender else rank + 1
-        pair = rank // 2
-        M = synth.d2_gradlike(n, m, 700 + pair)
-        E0 = synth.e0(n, m, 800 + pair, like=M)
-        Q0 = synth.q0(m, r, 9)
-        if peer < world:
-            if sender:
-                Md, Ed, Qd = (torch.from_numpy(x).to(dev) for x in (M, E0, Q0))
-                Pd = torch.empty(n, r, device=dev)
-                occ.occ_send_factors(Md, Ed, Qd, Pd, r, peer, comm)
-                own = torch.empty(n, m, device=dev)
-                occ.occ_decompress(Pd, Qd, own)          # what the sender's residual assumes
-                torch.cuda.synchronize()
-                dist.send(own, peer)
-                dist.send(Ed, peer)
+    # PP checks run twice: fp32 factors, and OCC_WIRE_BF16 (reading C7: bf16 factors on
+    # the wire, e_new against them; the oracle rounds its fp64 factors the same way,
+    # so a few elements may differ by one bf16 ulp -> 1e-3)
+    for wflags, sfx, wb, tolr in ((0, "", False, 1e-4), (occ.OCC_WIRE_BF16, "_wire_bf16", True, 1e-3)):
+        # ------------------------------------------------------------------ PP (pairs 1 -> 0, 3 -> 2, ...)
+        if world >= 2:
+            n, m, r = 2048, 3072, 32      # BASELINE configs[2] shape class (8.3B hidden), shortened rows
+            sender = rank % 2 == 1
+            peer = rank - 1 if sender else rank + 1
+            pair = rank // 2
+            M = synth.d2_gradlike(n, m, 700 + pair)
+            E0 = synth.e0(n, m, 800 + pair, like=M)
+            Q0 = synth.q0(m, r, 9)
+            if peer < world:
+                if sender:
+                    Md, Ed, Qd = (torch.from_numpy(x).to(dev) for x in (M, E0, Q0))
+                    Pd = torch.empty(n, r, device=dev)
+                    occ.occ_send_factors(Md, Ed, Qd, Pd, r, peer, comm, flags=wflags)
+                    own = torch.empty(n, m, device=dev)
+                    occ.occ_decompress(Pd, Qd, own)          # what the sender's residual assumes
+                    torch.cuda.synchronize()
+                    dist.send(own, peer)
+                    dist.send(Ed, peer)
+                else:
+                    out = torch.empty(n, m, device=dev)
+                    Pr = torch.empty(n, r, device=dev)
+                    Qr = torch.empty(m, r, device=dev)
+                    occ.occ_recv_factors(out, Pr, Qr, r, peer, comm, flags=wflags)
+                    torch.cuda.synchronize()
+                    own, e_snd = torch.empty(n, m, device=dev), torch.empty(n, m, device=dev)
+                    dist.recv(own, peer)
+                    dist.recv(e_snd, peer)
+                    own, e_snd = own.cpu(), e_snd.cpu()
+                    o = oracle.compress_step(M, E0, Q0, wire_bf16=wb)
+                    A = M.astype(np.float64) + E0
+                    got = out.double().cpu().numpy()
+                    r_rel = rel(got, o["recon"], A)
+                    bit = bool(torch.equal(out.cpu(), own))
+                    ef = rel(got + e_snd.double().numpy(), A, A)   # sender's e_new + receiver's M' = A
+                    good = r_rel <= tolr and bit and ef <= 1e-6
+                    flag = torch.tensor([1 if good else 0], device=dev)
+            flags_t = torch.tensor([1], device=dev)
+            if peer < world and not sender:
+                flags_t = flag
+            dist.all_reduce(flags_t, op=dist.ReduceOp.MIN)
+            if rank == 0:
+                report("pp_send_recv" + sfx, recon_rel=r_rel, bitwise_equal_to_sender=bit, ef_identity=ef,
+                       ok=bool(flags_t.item()))
             else:
-                out = torch.empty(n, m, device=dev)
-                Pr = torch.empty(n, r, device=dev)
-                Qr = torch.empty(m, r, device=dev)
-                occ.occ_recv_factors(out, Pr, Qr, r, peer, comm)
-                torch.cuda.synchronize()
-                own, e_snd = torch.empty(n, m, device=dev), torch.empty(n, m, device=dev)
-                dist.recv(own, peer)
-                dist.recv(e_snd, peer)
-                own, e_snd = own.cpu(), e_snd.cpu()
-                o = oracle.compress_step(M, E0, Q0)
-                A = M.astype(np.float64) + E0
-                got = out.double().cpu().numpy()
-                r_rel = rel(got, o["recon"], A)
-                bit = bool(torch.equal(out.cpu(), own))
-                ef = rel(got + e_snd.double().numpy(), A, A)   # sender's e_new + receiver's M' = A
-                good = r_rel <= 1e-4 and bit and ef <= 1e-6
-                flag = torch.tensor([1 if good else 0], device=dev)
-        flags_t = torch.tensor([1], device=dev)
-        if peer < world and not sender:
-            flags_t = flag
-        dist.all_reduce(flags_t, op=dist.ReduceOp.MIN)
-        if rank == 0:
-            report("pp_send_recv", recon_rel=r_rel, bitwise_equal_to_sender=bit, ef_identity=ef,
-                   ok=bool(flags_t.item()))
-        else:
-            ok = ok and bool(flags_t.item())
+                ok = ok and bool(flags_t.item())
 
-    # ------------------------------------------------------------------ PP ring (1F1B steady state)
-    # every rank compresses its own gradient and sends the factors to rank - 1
-    # while receiving rank + 1's and decompressing them (occ_sendrecv_factors)
-    if world >= 2:
-        n, m, r = 1024, 3072, 16      # north-star target T
-        mats = [synth.d2_gradlike(n, m, 1100 + w) for w in range(world)]
-        errs = [synth.e0(n, m, 1200 + w, like=mats[w]) for w in range(world)]
-        Q0 = synth.q0(m, r, 17)
-        Md, Ed, Qd = (torch.from_numpy(x).to(dev) for x in (mats[rank], errs[rank], Q0))
-        Pd = torch.empty(n, r, device=dev)
-        out = torch.empty(n, m, device=dev)
-        Pr, Qr = torch.empty(n, r, device=dev), torch.empty(m, r, device=dev)
-        snd, rcv = (rank - 1) % world, (rank + 1) % world
-        occ.occ_sendrecv_factors(Md, Ed, Qd, Pd, r, snd, out, Pr, Qr, rcv, comm)
-        own = torch.empty(n, m, device=dev)
-        occ.occ_decompress(Pd, Qd, own)          # what this rank's residual assumes
-        torch.cuda.synchronize()
-        owns = gather_np(own)
-        o = oracle.compress_step(mats[rcv], errs[rcv], Q0)
-        A = mats[rcv].astype(np.float64) + errs[rcv]
-        got = out.double().cpu().numpy()
-        r_rel = rel(got, o["recon"], A)
-        bit = bool(np.array_equal(got, owns[rcv]))
-        good = torch.tensor([1 if (r_rel <= 1e-4 and bit) else 0], device=dev)
-        dist.all_reduce(good, op=dist.ReduceOp.MIN)
-        report("pp_ring_sendrecv", recon_rel=r_rel, bitwise_equal_to_sender=bit, ok=bool(good.item()))
+        # ------------------------------------------------------------------ PP ring (1F1B steady state)
+        # every rank compresses its own gradient and sends the factors to rank - 1
+        # while receiving rank + 1's and decompressing them (occ_sendrecv_factors)
+        if world >= 2:
+            n, m, r = 1024, 3072, 16      # north-star target T
+            mats = [synth.d2_gradlike(n, m, 1100 + w) for w in range(world)]
+            errs = [synth.e0(n, m, 1200 + w, like=mats[w]) for w in range(world)]
+            Q0 = synth.q0(m, r, 17)
+            Md, Ed, Qd = (torch.from_numpy(x).to(dev) for x in (mats[rank], errs[rank], Q0))
+            Pd = torch.empty(n, r, device=dev)
+            out = torch.empty(n, m, device=dev)
+            Pr, Qr = torch.empty(n, r, device=dev), torch.empty(m, r, device=dev)
+            snd, rcv = (rank - 1) % world, (rank + 1) % world
+            occ.occ_sendrecv_factors(Md, Ed, Qd, Pd, r, snd, out, Pr, Qr, rcv, comm, flags=wflags)
+            own = torch.empty(n, m, device=dev)
+            occ.occ_decompress(Pd, Qd, own)          # what this rank's residual assumes
+            torch.cuda.synchronize()
+            owns = gather_np(own)
+            o = oracle.compress_step(mats[rcv], errs[rcv], Q0, wire_bf16=wb)
+            A = mats[rcv].astype(np.float64) + errs[rcv]
+            got = out.double().cpu().numpy()
+            r_rel = rel(got, o["recon"], A)
+            bit = bool(np.array_equal(got, owns[rcv]))
+            good = torch.tensor([1 if (r_rel <= tolr and bit) else 0], device=dev)
+            dist.all_reduce(good, op=dist.ReduceOp.MIN)
+            report("pp_ring_sendrecv" + sfx, recon_rel=r_rel, bitwise_equal_to_sender=bit, ok=bool(good.item()))
 
     # ------------------------------------------------------------------ EMB dense (fused, reading C12)
     V, h = 4096, 1024

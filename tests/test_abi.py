@@ -160,6 +160,17 @@ def test_allreduce_factors_rank_mismatch(L):
     assert status_name(L, s) == "OCC_ERR_RANK"
 
 
+def test_allreduce_factors_rejects_wire_bf16(L):
+    """OCC_WIRE_BF16 (reading C7) is defined for the PP send / recv calls only:
+    the DP exchange sums factors, so occ_allreduce_factors refuses it."""
+    M1, E1, Q1, P1 = good()
+    arr = occ.occ_mat * 1
+    rs = (ctypes.c_int * 1)(16)
+    s = L.occ_allreduce_factors(1, arr(M1), arr(E1), arr(Q1), arr(P1), rs, 1.0, occ.OCC_WIRE_BF16, None,
+                                ctypes.c_void_p(FAKE), 1 << 30, None)
+    assert status_name(L, s) == "OCC_ERR_UNSUPPORTED"
+
+
 def test_comm_null_handles(L):
     M, E, Q, P = good()
     s = L.occ_send_factors(M, E, Q, P, 16, 1, 0, None, ctypes.c_void_p(FAKE), 1 << 30, None)

@@ -189,23 +189,35 @@ def test_orient_t_matches_oracle(bf16, multi):
     g = {"P_hat": Pd.double().cpu().numpy(), "Q": Qd.double().cpu().numpy(), "recon": Rd.double().cpu().numpy(),
          "err": Ed.double().cpu().numpy()}
     check_step(g, o, M_used + e, tol=TOLBF if bf16 else TOL32)
+    out = torch.empty_like(Md)
+    occ.occ_decompress(Qd, Pd, out)   # M' = Q P^T in A's layout; bit-identical to the sender's (C8)
+    torch.cuda.synchronize()
+    assert torch.equal(out, Rd)
 
 
 @pytest.mark.parametrize("bf16", [False, True])
-def test_decompress_bit_identical_to_sender_reconstruction(bf16):
+@pytest.mark.parametrize("n,m,r,flags,path", [
+    (1000, 1208, 16, 0, 3),                      # fused kernel
+    (1000, 1208, 16, "FORCE_MULTI", 2),          # per-phase, multi-CTA Gram
+    (8192, 3072, 32, 0, 1),                      # per-phase: the fused kernel's tile plan does not fit
+    (640, 1024, 64, 0, 1),                       # r = 64 (v1 on both sides)
+])
+def test_decompress_bit_identical_to_sender_reconstruction(bf16, n, m, r, flags, path):
     """Reading C8: occ_decompress(P_hat, Q) on the receiver reproduces, bit for
-    bit, the M' the sender's e_new was taken against (same device arithmetic)."""
-    n, m, r = 1000, 1208, 16
+    bit, the M' the sender's e_new was taken against, whichever path compressed."""
     M = synth.d2_gradlike(n, m, 91)
     e = synth.e0(n, m, 92, like=M)
     Q0 = synth.q0(m, r, 93)
-    g = run_gpu(M, e, Q0, r, bf16=bf16)
-    assert g["stats"]["path"] == 3
+    g = run_gpu(M, e, Q0, r, bf16=bf16, flags=getattr(occ, "OCC_" + flags) if flags else 0)
+    assert g["stats"]["path"] == path
     Pd, Qd = to_dev(g["P_hat"]), to_dev(g["Q"])
     out = torch.empty(n, m, device="cuda", dtype=torch.bfloat16 if bf16 else torch.float32)
     occ.occ_decompress(Pd, Qd, out)
     torch.cuda.synchronize()
     assert np.array_equal(out.double().cpu().numpy(), g["recon"])
+    # and e_new was taken against that M' (fp32 rounding of A - M')
+    A32 = (g["M_used"].astype(np.float32) + e.astype(np.float32)).astype(np.float64)
+    assert np.abs(g["err"] + g["recon"] - A32).max() <= 1e-6 * np.abs(A32).max()
 
 
 # BASELINE.json configs at full size, in the launch configuration bench.py times
@@ -254,6 +266,49 @@ def test_check_finite_reports_nonfinite_input(monkeypatch, v1):
         occ.occ_check_status()
     assert exc.value.name == "OCC_ERR_NONFINITE"
     occ.occ_check_status()                                    # cleared by the report
+
+
+@pytest.mark.parametrize("mode", ["v2", "v1", "orient_t"])
+def test_wire_bf16(monkeypatch, mode):
+    """OCC_WIRE_BF16 (reading C7): P_hat and Q are bf16 values, the reconstruction
+    and e_new use them (vs the oracle with wire_bf16), and the receiver's
+    decompression of the bf16 factors is bit-identical to the sender's M' (C8)."""
+    n, m, r = 1000, 1208, 16
+    if mode == "v1":
+        monkeypatch.setenv("OCC_PATH", "v1")
+    ot = mode == "orient_t"
+    M = synth.d2_gradlike(n, m, 101)
+    e = synth.e0(n, m, 102, like=M)
+    Q0 = synth.q0(n if ot else m, r, 103)
+    flags = occ.OCC_WIRE_BF16 | (occ.OCC_ORIENT_T if ot else 0)
+    Md, Ed, Qd = to_dev(M), to_dev(e), to_dev(Q0)
+    Pd = torch.empty(m if ot else n, r, device="cuda")
+    Rd = torch.empty_like(Md)
+    ws = occ.occ_compress(Md, Ed, Qd, Pd, Rd, r=r, flags=flags)
+    torch.cuda.synchronize()
+    assert occ.occ_read_stats(ws)["path"] == {"v2": 3, "v1": 1, "orient_t": 1}[mode]
+    for t in (Pd, Qd):
+        assert torch.equal(t, t.to(torch.bfloat16).float())
+    o = oracle.compress_step(M, e, Q0, wire_bf16=True, orient_t=ot)
+    A = M.astype(np.float64) + e
+    g = {"P_hat": Pd.double().cpu().numpy(), "Q": Qd.double().cpu().numpy(), "recon": Rd.double().cpu().numpy(),
+         "err": Ed.double().cpu().numpy()}
+    # fp32-vs-fp64 factor differences can flip a bf16 rounding in a few
+    # elements (one bf16 ulp, 2^-8 relative): 1e-3 bounds that with margin.
+    assert rel(g["recon"], o["recon"], A) <= 1e-3
+    assert rel(g["err"], o["err"], A) <= 1e-3
+    assert rel(g["P_hat"], o["P_hat"], o["P_hat"]) <= TOLBF
+    assert rel(g["Q"], o["Q"], o["Q"]) <= TOLBF
+    assert np.linalg.norm(g["P_hat"].T @ g["P_hat"] - np.eye(r)) <= 1e-2   # orthonormal up to bf16 rounding
+    assert np.array_equal(g["recon"] + g["err"], A.astype(np.float32).astype(np.float64)) or \
+        np.abs(g["recon"] + g["err"] - A).max() <= 1e-5 * np.abs(A).max()
+    out = torch.empty_like(Md)
+    if ot:
+        occ.occ_decompress(Qd, Pd, out)
+    else:
+        occ.occ_decompress(Pd, Qd, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, Rd)
 
 
 def test_zero_input_all_fallbacks():

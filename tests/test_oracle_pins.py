@@ -300,3 +300,22 @@ def test_round_bf16_matches_torch_and_ties_to_even():
     np.testing.assert_array_equal(oracle.round_to(x.astype(np.float64), "bf16"), want)
     ties = np.array([1 + 2.0**-8, 1 + 3 * 2.0**-8, -(1 + 2.0**-8)])
     np.testing.assert_array_equal(oracle.round_to(ties, "bf16"), [1.0, 1 + 2.0**-6, -1.0])
+
+
+def test_wire_bf16_rounds_factors_to_bf16():
+    """Reading C7 (OCC_WIRE_BF16): the returned factors are bf16 values (the low
+    16 bits of their fp32 encoding are zero), each within half a bf16 ulp of
+    the fp64 factor (RNE), and the EF identity M' + e_new = A still holds."""
+    M = synth.d2_gradlike(64, 48, 1)
+    e = synth.e0(64, 48, 2, like=M)
+    Q0 = synth.q0(48, 4, 3)
+    a = oracle.compress_step(M, e, Q0)
+    b = oracle.compress_step(M, e, Q0, wire_bf16=True)
+    for key in ("P_hat", "Q"):
+        f32 = b[key].astype(np.float32)
+        assert np.array_equal(f32.astype(np.float64), b[key])
+        assert np.all((f32.view(np.uint32) & 0xFFFF) == 0)
+        ulp = np.ldexp(1.0, np.frexp(np.abs(a[key]))[1] - 8)   # bf16 spacing at |x|
+        assert np.all(np.abs(b[key] - a[key]) <= 0.5 * ulp + 1e-300)
+    A = M.astype(np.float64) + e
+    assert np.allclose(b["recon"] + b["err"], A, rtol=0, atol=1e-12)
