@@ -250,12 +250,15 @@ struct DecArgs {
   long long lde_out;
 };
 
+// row blocks per work item: 8, or 4 at r = 64 (the prefetched P fragment is RBI x r/8 x 2 registers)
+__host__ __device__ constexpr int dec_rbi(int r) { return r <= 32 ? 8 : 4; }
+
 template <int R, bool BF, bool EF>
 __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs d) {
   const float* __restrict__ P = d.P;
   const float* __restrict__ Q = d.Q;
   const int n = d.n, m = d.m;
-  constexpr int KS5 = K<R>::KS5, RBI = 8;
+  constexpr int KS5 = K<R>::KS5, RBI = dec_rbi(R);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int ncg = (m + 15) / 16, nrb = (n + 7) / 8;
   const int nitems = ncg * ((nrb + RBI - 1) / RBI);
@@ -583,7 +586,8 @@ unsigned take_nonfinite_v2() {
 }
 
 static cudaError_t launch_v2_decompress(const v2::DecArgs& d, int r, bool bf16, bool ef, cudaStream_t st) {
-  const int items = ((d.m + 15) / 16) * (((d.n + 7) / 8 + 7) / 8);
+  const int rbi = v2::dec_rbi(r);
+  const int items = ((d.m + 15) / 16) * (((d.n + 7) / 8 + rbi - 1) / rbi);
   const int grid = std::max(1, std::min((items + 7) / 8, 148 * 2));   // persistent: 2 CTAs per SM
   switch (r) {
 #define V2D(RR)                                                                                     \
@@ -596,7 +600,7 @@ static cudaError_t launch_v2_decompress(const v2::DecArgs& d, int r, bool bf16, 
       else v2::occ_v2_decompress_kernel<RR, false, false><<<grid, 256, 0, st>>>(d);                \
     }                                                                                               \
     return cudaGetLastError();
-    V2D(4) V2D(8) V2D(16) V2D(32)
+    V2D(4) V2D(8) V2D(16) V2D(32) V2D(64)
 #undef V2D
   }
   return cudaErrorNotSupported;
