@@ -269,30 +269,60 @@ def main():
     elif mode == "pp":
         launches_per_step = 2   # fused compress + decompress (NCCL's send/recv kernels are not ours)
 
-    # e2e through the public API with HOST buffers: H2D of M, the step, D2H of M'
+    # e2e through the public API with HOST buffers: every step copies its M in
+    # (pinned host -> device), runs the step and copies its M' out.  The copies
+    # run on their own streams with M and M' double-buffered on the device, so
+    # step k's D2H overlaps step k+1's H2D (PCIe is full duplex); the events
+    # order H2D -> step -> D2H per step and stop a buffer being overwritten
+    # before the step / copy that reads it has finished.
     Md, Ed, Qd, Pd, Rd, ws, Mkeep, Pr, Qr = res["bufs"]
     Mh = torch.from_numpy(make_inputs(n, m, seed=2000 + 10 * rank)[0]).pin_memory()
     Rh = torch.empty(n, m, dtype=torch.float32).pin_memory()
+    Mb = [Md, torch.empty_like(Md)]
+    Rb = [Rd, torch.empty_like(Rd)]
+    h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     e2e_steps = max(3, min(args.steps, 20))
-    e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
-    for i in range(e2e_steps + 2):
-        j = i - 2
-        if j >= 0:
-            e_ev[j][0].record(stream)
-        Md.copy_(Mh, non_blocking=True)
-        if dp:
-            occ.occ_allreduce_factors([Md], [Ed], [Qd], [Pd], RANK, 1.0 / world, comm=comm, ws=ws)
-            Rh.copy_(Md, non_blocking=True)
-        elif mode == "pp":
-            occ.occ_sendrecv_factors(Md, Ed, Qd, Pd, RANK, snd_peer, Rd, Pr, Qr, rcv_peer, comm, ws=ws)
-            Rh.copy_(Rd, non_blocking=True)
-        else:
-            occ.occ_compress(Md, Ed, Qd, Pd, Rd, r=RANK, ws=ws)
-            Rh.copy_(Rd, non_blocking=True)
-        if j >= 0:
-            e_ev[j][1].record(stream)
+
+    def e2e_run(k_steps):
+        ev = [[torch.cuda.Event() for _ in range(3)] for _ in range(k_steps)]   # H2D done, step done, D2H done
+        h2d_s.wait_stream(stream)   # the first copy starts after the caller's start event
+        for k in range(k_steps):
+            b = k % 2
+            if k >= 2:   # buffer b was last read by step k-2 (and, for DP, by its D2H)
+                h2d_s.wait_event(ev[k - 2][2] if dp else ev[k - 2][1])
+            with torch.cuda.stream(h2d_s):
+                Mb[b].copy_(Mh, non_blocking=True)
+            ev[k][0].record(h2d_s)
+            stream.wait_event(ev[k][0])
+            if k >= 2:
+                stream.wait_event(ev[k - 2][2])   # M'[b] of step k-2 copied out
+            if dp:
+                occ.occ_allreduce_factors([Mb[b]], [Ed], [Qd], [Pd], RANK, 1.0 / world, comm=comm, ws=ws)
+                out = Mb[b]
+            elif mode == "pp":
+                occ.occ_sendrecv_factors(Mb[b], Ed, Qd, Pd, RANK, snd_peer, Rb[b], Pr, Qr, rcv_peer, comm, ws=ws)
+                out = Rb[b]
+            else:
+                occ.occ_compress(Mb[b], Ed, Qd, Pd, Rb[b], r=RANK, ws=ws)
+                out = Rb[b]
+            ev[k][1].record(stream)
+            d2h_s.wait_event(ev[k][1])
+            with torch.cuda.stream(d2h_s):
+                Rh.copy_(out, non_blocking=True)
+            ev[k][2].record(d2h_s)
+        stream.wait_stream(d2h_s)
+        stream.wait_stream(h2d_s)
+
+    e2e_run(2)   # warm-up
     torch.cuda.synchronize()
-    e_tot = torch.tensor([sum(a.elapsed_time(b) for a, b in e_ev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    e2e_run(e2e_steps)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    e_tot = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e_tot, op=dist.ReduceOp.MAX)
     e_ms = e_tot.item() / e2e_steps
