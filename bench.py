@@ -138,10 +138,15 @@ def reference_arm(args):
     if rank != 0:
         return 0
     n, m = N_ROWS, N_COLS
-    run_oracle(n, m, args.warmup, 60.0)
-    dt, done = run_oracle(n, m, args.steps, 240.0)
+    # torchrun exports OMP_NUM_THREADS=1; rank 0 alone runs the oracle, so give it
+    # every host core it may use, as at N=1.
+    import numpy  # noqa: F401  (load its BLAS before the limit is raised)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=len(os.sched_getaffinity(0))):
+        run_oracle(n, m, args.warmup, 60.0)
+        dt, done = run_oracle(n, m, args.steps, 240.0)
+        cores = cpu_threads()
     gbs = n * m * 4 / dt / 1e9
-    cores = cpu_threads()
     line = {"impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": done, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
