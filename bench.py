@@ -283,8 +283,9 @@ def main():
     Md, Ed, Qd, Pd, Rd, ws, Mkeep, Pr, Qr = res["bufs"]
     Mh = torch.from_numpy(make_inputs(n, m, seed=2000 + 10 * rank)[0]).pin_memory()
     Rh = torch.empty(n, m, dtype=torch.float32).pin_memory()
-    Mb = [Md, torch.empty_like(Md)]
-    Rb = [Rd, torch.empty_like(Rd)]
+    nbuf = int(os.environ.get("OCC_E2E_NBUF", "2"))
+    Mb = [Md] + [torch.empty_like(Md) for _ in range(nbuf - 1)]
+    Rb = [Rd] + [torch.empty_like(Rd) for _ in range(nbuf - 1)]
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     e2e_steps = max(3, min(args.steps, 20))
 
@@ -292,15 +293,15 @@ def main():
         ev = [[torch.cuda.Event() for _ in range(3)] for _ in range(k_steps)]   # H2D done, step done, D2H done
         h2d_s.wait_stream(stream)   # the first copy starts after the caller's start event
         for k in range(k_steps):
-            b = k % 2
-            if k >= 2:   # buffer b was last read by step k-2 (and, for DP, by its D2H)
-                h2d_s.wait_event(ev[k - 2][2] if dp else ev[k - 2][1])
+            b = k % nbuf
+            if k >= nbuf:   # buffer b was last read by step k-nbuf (and, for DP, by its D2H)
+                h2d_s.wait_event(ev[k - nbuf][2] if dp else ev[k - nbuf][1])
             with torch.cuda.stream(h2d_s):
                 Mb[b].copy_(Mh, non_blocking=True)
             ev[k][0].record(h2d_s)
             stream.wait_event(ev[k][0])
-            if k >= 2:
-                stream.wait_event(ev[k - 2][2])   # M'[b] of step k-2 copied out
+            if k >= nbuf:
+                stream.wait_event(ev[k - nbuf][2])   # M'[b] of step k-nbuf copied out
             if dp:
                 occ.occ_allreduce_factors([Mb[b]], [Ed], [Qd], [Pd], RANK, 1.0 / world, comm=comm, ws=ws)
                 out = Mb[b]
