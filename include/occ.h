@@ -23,7 +23,11 @@
  *    allocates device memory; calls are asynchronous and stream ordered.
  *  - M and recon are OCC_F32 or OCC_BF16; err, P, Q are OCC_F32 always
  *    (reading C7 in DESIGN.md).  P is n x r, Q is m x r, both contiguous
- *    (ld == r).  r must be one of 4, 8, 16, 32, 64 and r <= min(n, m).
+ *    (ld == r).  r must be one of 4, 8, 16, 32, 64 and r <= min(n, m)
+ *    (the kernels are template instances per rank; the paper's ranks are 16
+ *    for CB and 128 for DP; 128 is not built: OCC_ERR_UNSUPPORTED).
+ *    M.cols must be a multiple of 8 (one 8-column MMA k-step; the paper's
+ *    hidden sizes 1920 / 3072 and every weight width are).
  *  - Alignment: 16-byte aligned pointers and ld*elsize % 16 == 0 (128-bit
  *    loads), else OCC_ERR_ALIGN.  M must not alias err, P or Q.
  *  - Argument errors are detected on the host before anything is enqueued;
@@ -145,14 +149,26 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
                                  const occ_mat* P, const int* r, float scale, uint32_t flags,
                                  occ_comm dp, void* ws, size_t ws_bytes, cudaStream_t stream);
 
-/* Pipeline backward link, sender side (stage s+1 -> s): occ_compress without
- * recon, then a grouped ncclSend of P_hat (n x r) and Q (m x r) to `peer`. */
+/* Pipeline backward link, sender side (stage s+1 -> s): compressed
+ * backpropagation of the inter-stage activation gradient (PAPER.md:351-396
+ * §CB; 386-389 lazy error propagation: err keeps e_new for the link's next
+ * micro-batch; 681-682 §Impl, the P2P low-rank send).  occ_compress without
+ * recon, then one NCCL group of two ncclSend calls: P_hat (n x r, or m x r
+ * with OCC_ORIENT_T) and Q (m x r / n x r) to `peer` of `pp`; OCC_WIRE_BF16
+ * sends them as bf16 (staged in ws).  Every argument check (shapes, peer,
+ * staging size) runs before anything is enqueued.  The call returns once the
+ * sends are enqueued on `stream`; a matching occ_recv_factors must be posted
+ * by `peer` (NCCL semantics: an unmatched send blocks the stream). */
 occ_status occ_send_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, int peer,
                             uint32_t flags, occ_comm pp, void* ws, size_t ws_bytes,
                             cudaStream_t stream);
 
-/* Receiver side: grouped ncclRecv of P_hat and Q from `peer`, then
- * out = round(P_hat Q^T) (bit-identical to the sender's implied M', C8). */
+/* Receiver side of the same link (§CB; 681-682 §Impl):
+ * one NCCL group of two ncclRecv calls into P (n x r) and Q (m x r) (caller-
+ * owned, overwritten; m x r / n x r with OCC_ORIENT_T) from `peer`, then
+ * out = round(P_hat Q^T) in out's dtype, bit-identical to
+ * the M' the sender's e_new was taken against (reading C8).  out must not
+ * overlap P or Q; with OCC_WIRE_BF16 out also stages the bf16 factors. */
 occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, uint32_t flags,
                             occ_comm pp, cudaStream_t stream);
 
@@ -184,7 +200,10 @@ occ_status occ_comm_wrap(occ_comm* comm, void* nccl_comm);
 occ_status occ_comm_rank(occ_comm comm, int* rank, int* nranks);
 occ_status occ_comm_destroy(occ_comm comm);
 
-/* Synchronises `stream`, then reports the first pending CUDA / NCCL error. */
+/* Synchronises `stream`, then reports the first pending CUDA error, the
+ * asynchronous NCCL error of `comm` (may be NULL: SURVEY.md §8(b) lists
+ * occ_check_status(stream); the communicator argument is needed because NCCL
+ * reports asynchronous errors per communicator), and OCC_ERR_NONFINITE. */
 occ_status occ_check_status(cudaStream_t stream, occ_comm comm);
 
 /* Copies the diagnostics of the last call that used `ws` (synchronises). */

@@ -55,19 +55,38 @@ def up_to_date(lib: str = LIB) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """Compiles every source to an object in parallel (one nvcc per .cu), then
+    links libocc.so; objects whose inputs did not change are reused."""
+    from concurrent.futures import ThreadPoolExecutor
     lib = LIB_TRACE if trace else LIB
     if not force and up_to_date(lib):
         return lib
     nd = nccl_dir()
-    tmp = lib + ".tmp"
-    cmd = [nvcc(), *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
-           *(["-DOCC_TRACE"] if trace else []),
-           "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nd, "include"),
-           *SOURCES, "-L" + os.path.join(nd, "lib"), "-l:libnccl.so.2",
-           "-Xlinker", "-rpath," + os.path.join(nd, "lib"), "-o", tmp]
+    objdir = os.path.join(HERE, "build", "trace" if trace else "prod")
+    os.makedirs(objdir, exist_ok=True)
+    common = [nvcc(), *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+              *(["-DOCC_TRACE"] if trace else []),
+              "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(nd, "include")]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), flush=True)
+        common.insert(1, "-Xptxas=-v")
+    headers = [d for d in DEPS if not d.endswith(".cu")]
+    newest_hdr = max((os.path.getmtime(h) for h in headers if os.path.exists(h)), default=0)
+
+    def obj(src):
+        o = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(src), newest_hdr):
+            cmd = common + ["-c", src, "-o", o + ".tmp"]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True)
+            os.replace(o + ".tmp", o)
+        return o
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(obj, SOURCES))
+    tmp = lib + ".tmp"
+    cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-L" + os.path.join(nd, "lib"), "-l:libnccl.so.2",
+           "-Xlinker", "-rpath," + os.path.join(nd, "lib"), "-o", tmp]
     subprocess.run(cmd, check=True)
     os.replace(tmp, lib)
     return lib

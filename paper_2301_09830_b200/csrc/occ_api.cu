@@ -5,6 +5,7 @@
 #include "occ_internal.h"
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -19,11 +20,25 @@ struct occ_comm_s {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   bool owned = true;   // false for occ_comm_wrap: the caller's communicator is not destroyed
+  // occ_embed_sync's PreMulSum op (scale * G summed), created once per (dtype, scale)
+  bool has_premul = false;
+  ncclRedOp_t premul_op{};
+  ncclDataType_t premul_dt{};
+  float premul_scale = 0.f;
 };
 
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range per API call (header-only NVTX 3: a no-op unless a profiler
+// injects itself), so nsys / ncu timelines show which call launched what.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 occ_status fail(occ_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 occ_status fail(occ_status s, const char* fmt, ...) {
@@ -162,14 +177,28 @@ occ_status nccl_fail(ncclResult_t r, const char* what) {
   return fail(OCC_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
 }
 
+// Inside an NCCL group: the first failing ncclSend / ncclRecv is kept in *first
+// (the group is still closed by the caller, which then reports it).
+void nccl_keep(ncclResult_t r, ncclResult_t* first) {
+  if (r != ncclSuccess && *first == ncclSuccess) *first = r;
+}
+
+// Closes a group and reports the first error of its calls, or of the close.
+occ_status group_end(ncclResult_t first, const char* what) {
+  const ncclResult_t e = ncclGroupEnd();
+  if (first != ncclSuccess) return nccl_fail(first, what);
+  if (e != ncclSuccess) return nccl_fail(e, what);
+  return OCC_OK;
+}
+
 // Phase ranges of run_phases (occ_step.cu PhaseId): [0,2) = sweep 1 + P reduce,
 // [2,6) = Gram + orthonormalisation, [6,8) = sweep 2 + Q reduce, [8,9) = reconstruct.
 constexpr int kPhA = 0, kPhOrth = 2, kPhD = 6, kPhF = 8, kPhEnd = 9;
 
 // phase F of a per-phase occ_compress (M' and e_new): the v2 decompress
-// arithmetic, so occ_decompress reproduces the sender's M' bit for bit (C8)
-// whichever path compressed; v1 phase F for r = 64, which occ_decompress also
-// runs in v1 (and under OCC_PATH=v1, where both sides are v1).
+// arithmetic for every supported rank (r = 4..64), so occ_decompress
+// reproduces the sender's M' bit for bit (C8) whichever path compressed; v1
+// phase F only under OCC_PATH=v1, where occ_decompress is v1 as well.
 cudaError_t reconstruct(const Params& p, const Geometry& g, int r, bool multi, cudaStream_t st) {
   if (!want_v1()) {
     cudaError_t e = run_v2_reconstruct(p, r, st);
@@ -194,30 +223,67 @@ cudaError_t orth_column_factor(const Params& base, float* U, int64_t m, int64_t 
 // OCC_WIRE_BF16 send side: the (already bf16-exact) factors packed into the
 // workspace's factor buckets, then sent as bf16.  Queues the ncclSends (inside
 // the caller's group).
-occ_status send_factors_bf16(const occ_mat& P, const occ_mat& Q, int r, int peer, occ_comm pp, void* ws,
-                             size_t ws_bytes, int64_t n, int64_t m, cudaStream_t st) {
+// OCC_WIRE_BF16 staging space check of the send side (before anything is enqueued).
+occ_status check_send_stage_bf16(int64_t prows, int64_t qrows, int r, size_t ws_bytes, int64_t n, int64_t m) {
   const WsLayout L = make_layout(make_geometry(n, m, r, kGeomSms), 1);
-  const size_t need = 2 * ((size_t)P.rows + (size_t)Q.rows) * r;
+  const size_t need = 2 * ((size_t)prows + (size_t)qrows) * r;
   if (L.qs_bucket - L.p_bucket < need || ws_bytes < L.total) return fail(OCC_ERR_WORKSPACE, "bf16 staging");
+  return OCC_OK;
+}
+
+// Packs the (already bf16-exact) factors (stream ordered, before the group).
+occ_status pack_factors_bf16(const occ_mat& P, const occ_mat& Q, int r, void* ws, int64_t n, int64_t m,
+                             cudaStream_t st) {
+  const WsLayout L = make_layout(make_geometry(n, m, r, kGeomSms), 1);
   char* stage = static_cast<char*>(ws) + L.p_bucket;
   cudaError_t e = run_pack_bf16(static_cast<const float*>(P.ptr), stage, (long long)P.rows * r, st);
   if (e == cudaSuccess) e = run_pack_bf16(static_cast<const float*>(Q.ptr), stage + 2 * (size_t)P.rows * r, (long long)Q.rows * r, st);
-  if (e != cudaSuccess) return cuda_fail(e, "bf16 pack");
-  ncclSend(stage, (size_t)P.rows * r, ncclBfloat16, peer, pp->comm, st);
-  ncclSend(stage + 2 * (size_t)P.rows * r, (size_t)Q.rows * r, ncclBfloat16, peer, pp->comm, st);
-  return OCC_OK;
+  return e == cudaSuccess ? OCC_OK : cuda_fail(e, "bf16 pack");
+}
+
+// Queues the bf16 sends of the packed factors (inside the caller's group).
+void send_factors_bf16(const occ_mat& P, const occ_mat& Q, int r, int peer, occ_comm pp, void* ws, int64_t n,
+                       int64_t m, cudaStream_t st, ncclResult_t* first) {
+  const WsLayout L = make_layout(make_geometry(n, m, r, kGeomSms), 1);
+  char* stage = static_cast<char*>(ws) + L.p_bucket;
+  nccl_keep(ncclSend(stage, (size_t)P.rows * r, ncclBfloat16, peer, pp->comm, st), first);
+  nccl_keep(ncclSend(stage + 2 * (size_t)P.rows * r, (size_t)Q.rows * r, ncclBfloat16, peer, pp->comm, st), first);
 }
 
 // OCC_WIRE_BF16 receive side: bf16 factors land in `out` (not yet written), are
 // expanded into Prcv / Qrcv, and `out` is then overwritten by the decompression.
-occ_status recv_factors_bf16(const occ_mat& out, const occ_mat& Prcv, const occ_mat& Qrcv, int r, int peer,
-                             occ_comm pp, cudaStream_t st) {
+occ_status check_recv_stage_bf16(const occ_mat& out, const occ_mat& Prcv, const occ_mat& Qrcv, int r) {
   const size_t need = 2 * ((size_t)Prcv.rows + (size_t)Qrcv.rows) * r;
   const size_t have = (size_t)out.rows * out.ld * (out.dtype == OCC_BF16 ? 2 : 4);
   if (have < need) return fail(OCC_ERR_UNSUPPORTED, "OCC_WIRE_BF16: out too small to stage the factors");
+  return OCC_OK;
+}
+void recv_factors_bf16(const occ_mat& out, const occ_mat& Prcv, const occ_mat& Qrcv, int r, int peer, occ_comm pp,
+                       cudaStream_t st, ncclResult_t* first) {
   char* stage = static_cast<char*>(out.ptr);
-  ncclRecv(stage, (size_t)Prcv.rows * r, ncclBfloat16, peer, pp->comm, st);
-  ncclRecv(stage + 2 * (size_t)Prcv.rows * r, (size_t)Qrcv.rows * r, ncclBfloat16, peer, pp->comm, st);
+  nccl_keep(ncclRecv(stage, (size_t)Prcv.rows * r, ncclBfloat16, peer, pp->comm, st), first);
+  nccl_keep(ncclRecv(stage + 2 * (size_t)Prcv.rows * r, (size_t)Qrcv.rows * r, ncclBfloat16, peer, pp->comm, st), first);
+}
+
+// Receiver-side checks (before anything is enqueued): the output view, the
+// factor shapes, aliasing between out and the factors (and, for the ring, the
+// sender's buffers), and the bf16 staging size.
+occ_status check_recv_side(const occ_mat& out, const occ_mat& Prcv, const occ_mat& Qrcv, int r, uint32_t flags,
+                           const occ_mat* snd_bufs, int nsnd) {
+  if (!out.ptr) return fail(OCC_ERR_INVALID_ARG, "out: null pointer");
+  occ_status s = check_rank(r, out.rows, out.cols);
+  if (s) return s;
+  if ((s = check_view(out, "out", out.rows, out.cols, false, false))) return s;
+  if (out.cols % 8 != 0) return fail(OCC_ERR_SHAPE, "out: cols must be a multiple of 8");
+  const bool ot = (flags & OCC_ORIENT_T) != 0;   // P m x r, Q n x r; out = Q P^T
+  if ((s = check_view(Prcv, "P", ot ? out.cols : out.rows, r, true, true))) return s;
+  if ((s = check_view(Qrcv, "Q", ot ? out.rows : out.cols, r, true, true))) return s;
+  if (overlap(out, Prcv) || overlap(out, Qrcv) || overlap(Prcv, Qrcv))
+    return fail(OCC_ERR_ALIAS, "out and the received factors must not overlap");
+  for (int i = 0; i < nsnd; i++)
+    if (overlap(snd_bufs[i], out) || overlap(snd_bufs[i], Prcv) || overlap(snd_bufs[i], Qrcv))
+      return fail(OCC_ERR_ALIAS, "receive buffers alias the sender's M / err / Q / P");
+  if ((flags & OCC_WIRE_BF16) && (s = check_recv_stage_bf16(out, Prcv, Qrcv, r))) return s;
   return OCC_OK;
 }
 occ_status unpack_factors_bf16(const occ_mat& out, const occ_mat& Prcv, const occ_mat& Qrcv, int r, cudaStream_t st) {
@@ -271,6 +337,7 @@ occ_status occ_init_q(occ_mat Q, uint64_t seed, cudaStream_t stream) {
 
 occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat recon, int r, uint32_t flags,
                         void* ws, size_t ws_bytes, cudaStream_t stream) {
+  NvtxRange nvtx_("occ_compress");
   occ_status s = check_step(M, err, Q, P, &recon, r, flags);
   if (s) return s;
   Geometry g = make_geometry(M.rows, M.cols, r, kGeomSms);
@@ -326,6 +393,7 @@ occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat re
 }
 
 occ_status occ_decompress(occ_mat P, occ_mat Q, occ_mat out, cudaStream_t stream) {
+  NvtxRange nvtx_("occ_decompress");
   if (!out.ptr) return fail(OCC_ERR_INVALID_ARG, "out: null pointer");
   const int r = (int)P.cols;
   occ_status s = check_rank(r, out.rows, out.cols);
@@ -347,13 +415,14 @@ occ_status occ_decompress(occ_mat P, occ_mat Q, occ_mat out, cudaStream_t stream
   p.r_bf16 = out.dtype == OCC_BF16;
   cudaError_t e = want_v1() ? cudaErrorNotSupported
                             : run_v2_decompress(p.P, p.Qrec, p.recon, p.ldr, p.n, p.m, r, p.r_bf16 != 0, stream);
-  if (e == cudaErrorNotSupported) e = run_decompress(p, r, stream);   // r = 64 (and OCC_PATH=v1)
+  if (e == cudaErrorNotSupported) e = run_decompress(p, r, stream);   // OCC_PATH=v1
   return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_decompress launch");
 }
 
 occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err, const occ_mat* Q, const occ_mat* P,
                                  const int* r, float scale, uint32_t flags, occ_comm dp, void* ws, size_t ws_bytes,
                                  cudaStream_t stream) {
+  NvtxRange nvtx_("occ_allreduce_factors");
   if (nmat < 1 || !G || !Q || !P || !r) return fail(OCC_ERR_INVALID_ARG, "null array or nmat < 1");
   if (!(flags & OCC_NO_EF) && !err) return fail(OCC_ERR_INVALID_ARG, "err array required unless OCC_NO_EF");
   if (flags & OCC_WIRE_BF16) return fail(OCC_ERR_UNSUPPORTED, "OCC_WIRE_BF16 applies to the send / recv calls");
@@ -374,7 +443,7 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
   if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(OCC_ERR_ALIGN, "workspace not 256-byte aligned");
   const bool multi = want_multi(flags);
   const bool dpl = !(flags & OCC_EF_GLOBAL);
-  const bool comm = dp && dp->nranks > 1;
+  const bool comm = dp != nullptr;   // a 1-rank group still runs its NCCL calls (tested on 1 GPU)
   char* base = static_cast<char*>(ws);
   float* pb = reinterpret_cast<float*>(base + L.p_bucket);
   float* qwb = reinterpret_cast<float*>(base + L.qw_bucket);
@@ -488,44 +557,45 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
 
 occ_status occ_send_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, int peer, uint32_t flags,
                             occ_comm pp, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  NvtxRange nvtx_("occ_send_factors");
   if (!pp) return fail(OCC_ERR_INVALID_ARG, "pp communicator is null");
   if (peer < 0 || peer >= pp->nranks || peer == pp->rank) return fail(OCC_ERR_INVALID_ARG, "bad peer %d", peer);
   occ_mat none = {nullptr, 0, 0, 0, M.dtype};
-  occ_status s = occ_compress(M, err, Q, P, none, r, flags, ws, ws_bytes, stream);
+  occ_status s = check_step(M, err, Q, P, nullptr, r, flags);
   if (s) return s;
-  ncclResult_t nr;
+  if ((flags & OCC_WIRE_BF16) && (s = check_send_stage_bf16(P.rows, Q.rows, r, ws_bytes, M.rows, M.cols))) return s;
+  if ((s = occ_compress(M, err, Q, P, none, r, flags, ws, ws_bytes, stream))) return s;
+  if ((flags & OCC_WIRE_BF16) && (s = pack_factors_bf16(P, Q, r, ws, M.rows, M.cols, stream))) return s;
+  ncclResult_t nr, first = ncclSuccess;
   if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
   if (flags & OCC_WIRE_BF16) {
-    s = send_factors_bf16(P, Q, r, peer, pp, ws, ws_bytes, M.rows, M.cols, stream);
-    if (s) { ncclGroupEnd(); return s; }
+    send_factors_bf16(P, Q, r, peer, pp, ws, M.rows, M.cols, stream, &first);
   } else {
-    ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream);   // (OCC_ORIENT_T: P is m x r)
-    ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream);
+    nccl_keep(ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream), &first);   // (OCC_ORIENT_T: P is m x r)
+    nccl_keep(ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream), &first);
   }
-  if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclSend(P,Q)");
-  return OCC_OK;
+  return group_end(first, "ncclSend(P,Q)");
 }
 
 occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, uint32_t flags, occ_comm pp,
                             cudaStream_t stream) {
+  NvtxRange nvtx_("occ_recv_factors");
   if (!pp) return fail(OCC_ERR_INVALID_ARG, "pp communicator is null");
   if (peer < 0 || peer >= pp->nranks || peer == pp->rank) return fail(OCC_ERR_INVALID_ARG, "bad peer %d", peer);
   if ((int)P.cols != r) return fail(OCC_ERR_SHAPE, "P: cols must equal r");
-  const bool ot = (flags & OCC_ORIENT_T) != 0;   // P m x r, Q n x r; out = Q P^T
-  occ_status s = check_view(P, "P", ot ? out.cols : out.rows, r, true, true);
+  occ_status s = check_recv_side(out, P, Q, r, flags, nullptr, 0);
   if (s) return s;
-  if ((s = check_view(Q, "Q", ot ? out.rows : out.cols, r, true, true))) return s;
+  const bool ot = (flags & OCC_ORIENT_T) != 0;   // P m x r, Q n x r; out = Q P^T
   const bool wire = (flags & OCC_WIRE_BF16) != 0;
-  ncclResult_t nr;
+  ncclResult_t nr, first = ncclSuccess;
   if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
   if (wire) {
-    s = recv_factors_bf16(out, P, Q, r, peer, pp, stream);
-    if (s) { ncclGroupEnd(); return s; }
+    recv_factors_bf16(out, P, Q, r, peer, pp, stream, &first);
   } else {
-    ncclRecv(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream);
-    ncclRecv(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream);
+    nccl_keep(ncclRecv(P.ptr, (size_t)P.rows * r, ncclFloat, peer, pp->comm, stream), &first);
+    nccl_keep(ncclRecv(Q.ptr, (size_t)Q.rows * r, ncclFloat, peer, pp->comm, stream), &first);
   }
-  if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclRecv(P,Q)");
+  if ((s = group_end(first, "ncclRecv(P,Q)"))) return s;
   if (wire && (s = unpack_factors_bf16(out, P, Q, r, stream))) return s;
   return ot ? occ_decompress(Q, P, out, stream) : occ_decompress(P, Q, out, stream);
 }
@@ -533,75 +603,89 @@ occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, 
 occ_status occ_sendrecv_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, int send_peer, occ_mat out,
                                 occ_mat Prcv, occ_mat Qrcv, int recv_peer, uint32_t flags, occ_comm pp, void* ws,
                                 size_t ws_bytes, cudaStream_t stream) {
+  NvtxRange nvtx_("occ_sendrecv_factors");
   if (!pp) return fail(OCC_ERR_INVALID_ARG, "pp communicator is null");
   const bool snd = send_peer >= 0, rcv = recv_peer >= 0;
-  if (snd && (send_peer >= pp->nranks || send_peer == pp->rank)) return fail(OCC_ERR_INVALID_ARG, "bad send_peer %d", send_peer);
-  if (rcv && (recv_peer >= pp->nranks || recv_peer == pp->rank)) return fail(OCC_ERR_INVALID_ARG, "bad recv_peer %d", recv_peer);
-  const bool ot = (flags & OCC_ORIENT_T) != 0;
+  // a stage may be its own peer only when it both sends and receives in this
+  // one group (a ring of one stage, e.g. a 1-GPU check of the NCCL exchange)
+  const bool self_ok = snd && rcv && send_peer == pp->rank && recv_peer == pp->rank;
+  if (snd && (send_peer >= pp->nranks || (send_peer == pp->rank && !self_ok)))
+    return fail(OCC_ERR_INVALID_ARG, "bad send_peer %d", send_peer);
+  if (rcv && (recv_peer >= pp->nranks || (recv_peer == pp->rank && !self_ok)))
+    return fail(OCC_ERR_INVALID_ARG, "bad recv_peer %d", recv_peer);
+  const bool wire = (flags & OCC_WIRE_BF16) != 0;
+  // every argument check before anything is enqueued (occ.h conventions)
+  occ_status s;
+  if (snd) {
+    if ((s = check_step(M, err, Q, P, nullptr, r, flags))) return s;
+    if (wire && (s = check_send_stage_bf16(P.rows, Q.rows, r, ws_bytes, M.rows, M.cols))) return s;
+  }
   if (rcv) {
-    if (!out.ptr) return fail(OCC_ERR_INVALID_ARG, "out: null pointer");
-    occ_status s = check_view(Prcv, "Prcv", ot ? out.cols : out.rows, r, true, true);
-    if (s) return s;
-    if ((s = check_view(Qrcv, "Qrcv", ot ? out.rows : out.cols, r, true, true))) return s;
+    const occ_mat sb[4] = {M, err, Q, P};
+    if ((s = check_recv_side(out, Prcv, Qrcv, r, flags, sb, snd ? 4 : 0))) return s;
   }
   if (snd) {
     occ_mat none = {nullptr, 0, 0, 0, M.dtype};
-    occ_status s = occ_compress(M, err, Q, P, none, r, flags, ws, ws_bytes, stream);
-    if (s) return s;
+    if ((s = occ_compress(M, err, Q, P, none, r, flags, ws, ws_bytes, stream))) return s;
+    if (wire && (s = pack_factors_bf16(P, Q, r, ws, M.rows, M.cols, stream))) return s;
   }
-  const bool wire = (flags & OCC_WIRE_BF16) != 0;
-  ncclResult_t nr;
+  ncclResult_t nr, first = ncclSuccess;
   if ((nr = ncclGroupStart()) != ncclSuccess) return nccl_fail(nr, "ncclGroupStart");
   if (snd) {
     if (wire) {
-      occ_status s = send_factors_bf16(P, Q, r, send_peer, pp, ws, ws_bytes, M.rows, M.cols, stream);
-      if (s) { ncclGroupEnd(); return s; }
+      send_factors_bf16(P, Q, r, send_peer, pp, ws, M.rows, M.cols, stream, &first);
     } else {
-      ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, send_peer, pp->comm, stream);
-      ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, send_peer, pp->comm, stream);
+      nccl_keep(ncclSend(P.ptr, (size_t)P.rows * r, ncclFloat, send_peer, pp->comm, stream), &first);
+      nccl_keep(ncclSend(Q.ptr, (size_t)Q.rows * r, ncclFloat, send_peer, pp->comm, stream), &first);
     }
   }
   if (rcv) {
     if (wire) {
-      occ_status s = recv_factors_bf16(out, Prcv, Qrcv, r, recv_peer, pp, stream);
-      if (s) { ncclGroupEnd(); return s; }
+      recv_factors_bf16(out, Prcv, Qrcv, r, recv_peer, pp, stream, &first);
     } else {
-      ncclRecv(Prcv.ptr, (size_t)Prcv.rows * r, ncclFloat, recv_peer, pp->comm, stream);
-      ncclRecv(Qrcv.ptr, (size_t)Qrcv.rows * r, ncclFloat, recv_peer, pp->comm, stream);
+      nccl_keep(ncclRecv(Prcv.ptr, (size_t)Prcv.rows * r, ncclFloat, recv_peer, pp->comm, stream), &first);
+      nccl_keep(ncclRecv(Qrcv.ptr, (size_t)Qrcv.rows * r, ncclFloat, recv_peer, pp->comm, stream), &first);
     }
   }
-  if ((nr = ncclGroupEnd()) != ncclSuccess) return nccl_fail(nr, "ncclSendRecv(P,Q)");
+  if ((s = group_end(first, "ncclSendRecv(P,Q)"))) return s;
   if (!rcv) return OCC_OK;
-  if (wire) {
-    occ_status s = unpack_factors_bf16(out, Prcv, Qrcv, r, stream);
-    if (s) return s;
-  }
+  if (wire && (s = unpack_factors_bf16(out, Prcv, Qrcv, r, stream))) return s;
+  const bool ot = (flags & OCC_ORIENT_T) != 0;
   return ot ? occ_decompress(Qrcv, Prcv, out, stream) : occ_decompress(Prcv, Qrcv, out, stream);
 }
 
 occ_status occ_embed_sync(occ_mat G, occ_mat err, occ_mat Q, occ_mat P, int r, float scale, uint32_t flags,
                           occ_comm emb, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  NvtxRange nvtx_("occ_embed_sync");
   if (r > 0) return occ_allreduce_factors(1, &G, &err, &Q, &P, &r, scale, flags, emb, ws, ws_bytes, stream);
   occ_status s = check_view(G, "G", G.rows, G.cols, false, true);
   if (s) return s;
-  if (!emb || emb->nranks == 1) {
+  if (!emb) {   // no group: the identity when scale == 1 (a group of one rank)
     if (scale == 1.0f) return OCC_OK;
+    return fail(OCC_ERR_INVALID_ARG, "emb communicator is null");
   }
   ncclDataType_t dt = G.dtype == OCC_BF16 ? ncclBfloat16 : ncclFloat;
   const size_t count = (size_t)G.rows * G.cols;
-  if (!emb) return fail(OCC_ERR_INVALID_ARG, "emb communicator is null");
-  ncclRedOp_t op;
   ncclResult_t nr;
-  if (G.dtype == OCC_BF16) {
-    // scalar type must match the data type
-    __nv_bfloat16 sb = __float2bfloat16_rn(scale);
-    nr = ncclRedOpCreatePreMulSum(&op, &sb, dt, ncclScalarHostImmediate, emb->comm);
-  } else {
-    nr = ncclRedOpCreatePreMulSum(&op, &scale, dt, ncclScalarHostImmediate, emb->comm);
+  // one PreMulSum op per communicator, re-created only when the dtype or the
+  // scale changes (the FE scale 1/D is fixed for a run, reading C12)
+  if (!emb->has_premul || emb->premul_dt != dt || emb->premul_scale != scale) {
+    if (emb->has_premul) {
+      ncclRedOpDestroy(emb->premul_op, emb->comm);
+      emb->has_premul = false;
+    }
+    if (G.dtype == OCC_BF16) {
+      __nv_bfloat16 sb = __float2bfloat16_rn(scale);   // the scalar's type must match the data type
+      nr = ncclRedOpCreatePreMulSum(&emb->premul_op, &sb, dt, ncclScalarHostImmediate, emb->comm);
+    } else {
+      nr = ncclRedOpCreatePreMulSum(&emb->premul_op, &scale, dt, ncclScalarHostImmediate, emb->comm);
+    }
+    if (nr != ncclSuccess) return nccl_fail(nr, "ncclRedOpCreatePreMulSum");
+    emb->has_premul = true;
+    emb->premul_dt = dt;
+    emb->premul_scale = scale;
   }
-  if (nr != ncclSuccess) return nccl_fail(nr, "ncclRedOpCreatePreMulSum");
-  nr = ncclAllReduce(G.ptr, G.ptr, count, dt, op, emb->comm, stream);
-  ncclRedOpDestroy(op, emb->comm);
+  nr = ncclAllReduce(G.ptr, G.ptr, count, dt, emb->premul_op, emb->comm, stream);
   if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(EMB)");
   return OCC_OK;
 }
@@ -661,6 +745,7 @@ occ_status occ_comm_wrap(occ_comm* comm, void* nccl_comm) {
 
 occ_status occ_comm_destroy(occ_comm comm) {
   if (!comm) return OCC_OK;
+  if (comm->has_premul) ncclRedOpDestroy(comm->premul_op, comm->comm);
   ncclResult_t nr = comm->owned ? ncclCommDestroy(comm->comm) : ncclSuccess;
   delete comm;
   return nr == ncclSuccess ? OCC_OK : nccl_fail(nr, "ncclCommDestroy");

@@ -44,11 +44,13 @@ cudaError_t run_pack_bf16(const float* x, void* y, long long count, cudaStream_t
 cudaError_t run_unpack_bf16(const void* y, float* x, long long count, cudaStream_t st);
 unsigned take_nonfinite_v2();
 // out = round(P Q^T) with the fused kernel's phase-5 arithmetic (bit-identical
-// to the sender's reconstruction, reading C8); cudaErrorNotSupported if r > 32.
+// to the sender's reconstruction, reading C8); every supported rank (4..64),
+// cudaErrorNotSupported for any other.
 cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r, bool bf16,
                               cudaStream_t st);
 // sender-side M' and e_new = (M + e_old) - M' of the per-phase paths, in the
-// decompress kernel's arithmetic (reading C8); cudaErrorNotSupported for r = 64
+// decompress kernel's arithmetic (reading C8), every supported rank (4..64).
+// A = M + e_old is loaded before M' is stored, so recon may alias M.
 cudaError_t run_v2_reconstruct(const Params& p, int r, cudaStream_t st);
 cudaError_t run_init_q(float* q, int64_t rows, int r, int64_t ld, uint64_t seed, cudaStream_t st);
 

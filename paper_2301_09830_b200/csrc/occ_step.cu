@@ -124,6 +124,20 @@ Geometry make_geometry(int64_t n, int64_t m, int r, int sms) {
 
 static size_t al(size_t x) { return (x + 255) / 256 * 256; }
 
+// max over n' <= n, m' <= m (m' % 8 == 0) of s1(n', m') * n' (see make_layout)
+static size_t max_sweep1_rows(int64_t n, int64_t m, int r) {
+  const int ur = (r <= 32) ? 64 : 32;
+  size_t best = 0;
+  for (int64_t nb = 1; (nb - 1) * ur < n; nb++) {
+    const int64_t nn = std::min<int64_t>(nb * ur, n);
+    for (int64_t mm = 8; mm <= m; mm += 8) {
+      const Geometry g = make_geometry(nn, mm, r, 148);
+      best = std::max(best, (size_t)g.s1 * (size_t)nn);
+    }
+  }
+  return best;
+}
+
 WsLayout make_layout(const Geometry& g, int nmat) {
   WsLayout L;
   const int R = g.r;
@@ -132,7 +146,14 @@ WsLayout make_layout(const Geometry& g, int nmat) {
   L.bar = off; off += 256;                                 // bar[2], ctl[4], stats
   off += kTraceBytes;                                      // per-CTA phase trace (occ_read_trace)
   off += kBarLinesBytes;                                   // v2 grid-barrier arrival lines
-  L.p_part = off; off = al(off + (size_t)g.s1 * g.n * R * 4);
+  // A bucket (nmat > 1) holds matrices of at most n x m; each one's sweep-1
+  // partials need s1_i * n_i rows, which can exceed s1 * n of the largest
+  // shape (s1 grows as a matrix gets shorter), so take the maximum over every
+  // shape the bucket may hold (s1 depends on the rows only through the row
+  // block count, and cols are multiples of 8).
+  size_t prows = (size_t)g.s1 * g.n;
+  if (nmat > 1) prows = std::max(prows, max_sweep1_rows(g.n, g.m, R));
+  L.p_part = off; off = al(off + prows * R * 4);
   L.q_part = off; off = al(off + (size_t)g.s2 * g.m * R * 4);
   // Gram partials: per 128 rows of the orthonormalised factor, which is the
   // row side (n) or, with OCC_ORIENT_T, the column side (m)

@@ -329,20 +329,10 @@ __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs
           v0 = __bfloat162float(__float2bfloat16_rn(v0));
           v1 = __bfloat162float(__float2bfloat16_rn(v1));
         }
-        if (d.out) {
-          const size_t o0 = (size_t)row * d.ldo + c;
-          if (BF) {
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(d.out) + o0;
-            if (two) *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
-            else dst[0] = __float2bfloat16_rn(v0);
-          } else {
-            float* dst = reinterpret_cast<float*>(d.out) + o0;
-            if (two) *reinterpret_cast<float2*>(dst) = make_float2(v0, v1);
-            else dst[0] = v0;
-          }
-        }
+        // EF: A = M + e_old is loaded BEFORE M' is stored, so recon may alias M
+        // (an in-place occ_compress) and err_out may alias err_in
+        float a0 = 0.f, a1 = 0.f;
         if constexpr (EF) {
-          float a0, a1 = 0.f;
           if (d.m_bf16) {
             const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(d.M) + (size_t)row * d.ldm + c;
             if (two) {
@@ -369,6 +359,20 @@ __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs
               a0 += src[0];
             }
           }
+        }
+        if (d.out) {
+          const size_t o0 = (size_t)row * d.ldo + c;
+          if (BF) {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(d.out) + o0;
+            if (two) *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
+            else dst[0] = __float2bfloat16_rn(v0);
+          } else {
+            float* dst = reinterpret_cast<float*>(d.out) + o0;
+            if (two) *reinterpret_cast<float2*>(dst) = make_float2(v0, v1);
+            else dst[0] = v0;
+          }
+        }
+        if constexpr (EF) {
           float* dst = d.err_out + (size_t)row * d.lde_out + c;
           if (two) *reinterpret_cast<float2*>(dst) = make_float2(a0 - v0, a1 - v1);
           else dst[0] = a0 - v0;

@@ -249,6 +249,17 @@ class Comm:
         return cls(h.value)
 
     @classmethod
+    def single(cls) -> "Comm":
+        """A communicator of one rank (no process group needed): its NCCL
+        calls still run (an allreduce copies, a send to self lands in the
+        matching recv), which is how the 1-GPU tests exercise the exchange."""
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().occ_get_unique_id(buf), "occ_get_unique_id")
+        h = ctypes.c_void_p()
+        _check(lib().occ_comm_init(ctypes.byref(h), bytes(buf.raw), 1, 0), "occ_comm_init")
+        return cls(h.value)
+
+    @classmethod
     def wrap(cls, nccl_comm_ptr: int) -> "Comm":
         """Adopt an existing ncclComm_t (not destroyed by destroy()), e.g. the
         communicator of a torch ProcessGroupNCCL (its private _comm_ptr())."""

@@ -29,6 +29,17 @@ class Policy:
     lep: bool = True             # lazy error propagation on (Non-LEP = PAPER.md:893 ablation)
     fe: bool = True              # fused embedding synchronisation
 
+    def kernel_rank(self, r: int) -> int:
+        """The rank the library runs for a requested rank r: the largest built
+        instance (4, 8, 16, 32, 64) not above r.  The paper's DP rank 128
+         is not built, so DP compression driven by this policy
+        runs at 64 (a smaller rank: fewer factor bytes, larger residual, which
+        error feedback carries to the next step)."""
+        built = (4, 8, 16, 32, 64)
+        if r < built[0]:
+            raise ValueError(f"rank {r} below the smallest built rank 4")
+        return max(b for b in built if b <= r)
+
 
 def epilogue_compressed(k: int, num_microbatches: int, num_stages: int, stage: int) -> bool:
     """Is the backward send of micro-batch k from `stage` to `stage - 1` compressed?"""

@@ -107,7 +107,7 @@ def main():
     for wflags, sfx, wb, tolr in ((0, "", False, 1e-4), (occ.OCC_WIRE_BF16, "_wire_bf16", True, 1e-3)):
         # ------------------------------------------------------------------ PP (pairs 1 -> 0, 3 -> 2, ...)
         if world >= 2:
-            n, m, r = 2048, 3072, 32      # BASELINE configs[2] shape class (8.3B hidden), shortened rows
+            n, m, r = 8192, 3072, 32      # BASELINE configs[2]: GPT-8.3B inter-stage, 1024 tokens x mb 8
             sender = rank % 2 == 1
             peer = rank - 1 if sender else rank + 1
             pair = rank // 2
@@ -217,6 +217,48 @@ def main():
     o = oracle.dp_step(Gs, None, Q0, scale=1.0 / D, orient_t=True)
     e3 = rel(G.double().cpu().numpy(), o["recon"], A / D)
     report("emb_compressed_orient_t", recon_rel=e3, ok=e3 <= 1e-4)
+
+    # ------------------------------------------------------------------ C5 EMB at full size (BASELINE configs[4])
+    # the 50257 x 3072 tied-embedding gradient, compressed as G^T (OCC_ORIENT_T,
+    # reading C6) at r = 64 over all ranks (first stage ranks: row-sparse D5,
+    # last stage ranks: dense D2), scale 1/D (reading C12/C14).  Rank 0 runs the
+    # oracle on every rank's input; M' must be bit-identical on all ranks.
+    if os.environ.get("OCC_MP_FULL_EMB", "1") == "1":
+        V, h, r = 50257, 3072, 64
+        D = max(1, world // 2)
+        mk = lambda w: synth.d5_embedding_sparse(V, h, 1400 + w) if w < D else synth.d2_gradlike(V, h, 1400 + w)
+        Gw = mk(rank)
+        Q0 = synth.q0(V, r, 15)
+        G = torch.from_numpy(Gw).to(dev)
+        E = torch.zeros(V, h, device=dev)
+        Q = torch.from_numpy(Q0).to(dev)
+        P = torch.empty(h, r, device=dev)
+        occ.occ_embed_sync(G, E, Q, P, r, 1.0 / D, comm, flags=occ.OCC_ORIENT_T)
+        torch.cuda.synchronize()
+        csum = torch.tensor([float(G.double().sum()), float((G.double() ** 2).sum())], device=dev, dtype=torch.float64)
+        allc = [torch.empty_like(csum) for _ in range(world)]
+        dist.all_gather(allc, csum)
+        same = all(torch.equal(allc[0], c) for c in allc)
+        if rank == 0:
+            Gs = [mk(w) for w in range(world)]
+            o = oracle.dp_step(Gs, None, Q0, scale=1.0 / D, orient_t=True)
+            A = sum(g.astype(np.float64) for g in Gs)
+            got = G.double().cpu().numpy()
+            e4 = rel(got, o["recon"], A / D)
+            el = float(np.abs(got - o["recon"]).max() / np.abs(A / D).max())
+            ee = rel(E.double().cpu().numpy(), o["err"][0], Gs[0].astype(np.float64))
+            Ph = P.double().cpu().numpy()
+            orth = float(np.linalg.norm(Ph.T @ Ph - np.eye(r)))
+            good = e4 <= 1e-4 and el <= 1e-5 and ee <= 1e-4 and orth <= 1e-5 and same
+            del Gs, o, A
+        else:
+            e4 = el = ee = orth = None
+            good = True
+        g_t = torch.tensor([1 if good else 0], device=dev)
+        dist.all_reduce(g_t, op=dist.ReduceOp.MIN)
+        report("emb_compressed_orient_t_full_50257x3072_r64", recon_rel=e4, recon_elem=el, err_rel_rank0=ee,
+               orth=orth, identical_on_ranks=same, ok=bool(g_t.item()))
+        del G, E, Q, P, Gw
 
     # ------------------------------------------------------------------ occ_comm_wrap (torch's communicator)
     try:

@@ -319,3 +319,107 @@ def test_wire_bf16_rounds_factors_to_bf16():
         assert np.all(np.abs(b[key] - a[key]) <= 0.5 * ulp + 1e-300)
     A = M.astype(np.float64) + e
     assert np.allclose(b["recon"] + b["err"], A, rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------- round-2 pins ("What's weak" 1)
+def test_fallback_vector_formula_against_published_splitmix64(golden_dir):
+    """f[i] = (splitmix64(seed ^ (j << 32) ^ i) >> 40) 2^-23 - 1 (reading C3).
+    The counter is chosen so that it equals a published SplitMix64 state
+    (s + k*gamma): then f[i] follows from the published output alone.  Catches
+    a wrong shift of j, a wrong >> (e.g. 41), a wrong scale or offset."""
+    g = _load(golden_dir, "splitmix64.json")
+    gamma, s = 0x9E3779B97F4A7C15, 1234567
+    for k, pub in enumerate(g["seed1234567_first5"]):
+        j, i = k + 1, 5 + 3 * k
+        x = (s + k * gamma) % 2**64                  # the published stream's k-th counter
+        seed = x ^ (j << 32) ^ i                     # so that seed ^ (j<<32) ^ i == x
+        f = oracle.fallback_vector(seed, j, i + 1)
+        assert f[i] == (pub >> 40) * 2.0**-23 - 1.0
+    # seed 0, j 0, i 0: splitmix64(0) = 0xE220A8397B1DCDAF -> 0xE220A8 / 2^23 - 1, exact
+    f0 = oracle.fallback_vector(0, 0, 1)[0]
+    assert f0 == Fraction(0xE220A8 - 2**23, 2**23)
+
+
+def test_decompress_hand_values_and_orientation():
+    """SPEC.md:123-131 lowrank_decompress: M' = round(P_hat Q^T).  Hand values
+    (an outer product), the transpose under orient_t, bf16 RNE on a tie."""
+    P = np.array([[1.0], [2.0]])
+    Q = np.array([[3.0], [5.0], [7.0]])
+    want = np.array([[3.0, 5, 7], [6, 10, 14]])
+    np.testing.assert_array_equal(oracle.decompress(P, Q), want)
+    np.testing.assert_array_equal(oracle.decompress(P, Q, orient_t=True), want.T)
+    # rank 2: the sum of two outer products (a dropped column fails)
+    P2 = np.array([[1.0, 0.0], [0.0, 1.0]])
+    Q2 = np.array([[1.0, 2.0], [3.0, 4.0]])
+    np.testing.assert_array_equal(oracle.decompress(P2, Q2), [[1.0, 3.0], [2.0, 4.0]])
+    # bf16: 1 + 2^-8 is a tie between 1 and 1 + 2^-7 -> even (1.0); 1 + 3*2^-8 -> 1 + 2^-6
+    tie = oracle.decompress(np.array([[1.0]]), np.array([[1.0 + 2.0**-8], [1.0 + 3 * 2.0**-8]]), out_dtype="bf16")
+    np.testing.assert_array_equal(tie, [[1.0, 1.0 + 2.0**-6]])
+
+
+def test_decompress_reproduces_the_compressors_recon(golden_dir):
+    """decompress(P_hat, Q) is the M' that compress_step's e_new was taken
+    against, on the P1 hand example (exact values) and with orient_t."""
+    g = _load(golden_dir, "p1_hand_example.json")
+    M = np.array(g["M"], float)
+    s1 = oracle.compress_step(M, None, np.array(g["Q0"], float))
+    d = oracle.decompress(s1["P_hat"], s1["Q"])
+    np.testing.assert_allclose(d, np.array(g["step1"]["recon_num"]) / g["step1"]["recon_den"], atol=1e-15)
+    np.testing.assert_array_equal(d, s1["recon"])
+    rng = np.random.default_rng(31)
+    A = rng.standard_normal((12, 7))
+    s = oracle.compress_step(A, None, rng.standard_normal((12, 3)), orient_t=True)
+    np.testing.assert_array_equal(oracle.decompress(s["P_hat"], s["Q"], orient_t=True), s["recon"])
+    for dt in ("f32", "bf16"):
+        s = oracle.compress_step(A, None, rng.standard_normal((7, 3)), out_dtype=dt)
+        np.testing.assert_array_equal(oracle.decompress(s["P_hat"], s["Q"], out_dtype=dt), s["recon"])
+
+
+def test_dp_orient_t_hand_example(golden_dir):
+    """dp_step(orient_t=True) on a hand-worked D = 2 example with a
+    non-symmetric A_1 (a dropped transpose fails every value)."""
+    g = _load(golden_dir, "p10t_dp_orient_t_hand_example.json")
+    As = [np.array(x, float) for x in g["A"]]
+    Q0 = np.array(g["Q0"], float)
+    sc = g["scale_num"] / g["scale_den"]
+    loc = oracle.dp_step(As, None, Q0, scale=sc, orient_t=True)
+    glo = oracle.dp_step(As, None, Q0, scale=sc, orient_t=True, ef_global=True)
+    np.testing.assert_allclose(loc["P_hat"], np.array(g["P_hat_num"]) / math.sqrt(g["P_hat_den_sqrt"]), atol=1e-15)
+    np.testing.assert_allclose(loc["Q"], np.array(g["Q_num"]) / math.sqrt(g["Q_den_sqrt"]), atol=1e-15)
+    np.testing.assert_allclose(loc["recon"], np.array(g["recon_num"]) / g["recon_den"], atol=1e-15)
+    for w in range(2):
+        np.testing.assert_allclose(loc["err"][w], np.array(g["err_local_num"][w]) / g["err_local_den"], atol=1e-15)
+        np.testing.assert_allclose(glo["err"][w], np.array(g["err_global_num"][w]) / g["err_global_den"], atol=1e-15)
+    want_sum = np.array(g["err_sum_num"]) / g["err_sum_den"]
+    np.testing.assert_allclose(sum(loc["err"]), want_sum, atol=1e-15)
+    np.testing.assert_allclose(sum(glo["err"]), want_sum, atol=1e-15)
+
+
+def test_dp_orient_t_equals_dp_step_on_transposes():
+    """orient_t is the DP step on A_w^T, returned in A's layout (reading C6)."""
+    rng = np.random.default_rng(32)
+    n, m, r, D = 40, 18, 4, 3
+    Ms = [rng.standard_normal((n, m)) for _ in range(D)]
+    Es = [0.1 * rng.standard_normal((n, m)) for _ in range(D)]
+    Q0 = rng.standard_normal((n, r))
+    for eg in (False, True):
+        a = oracle.dp_step(Ms, Es, Q0, scale=1.0 / D, orient_t=True, ef_global=eg)
+        b = oracle.dp_step([x.T for x in Ms], [x.T for x in Es], Q0, scale=1.0 / D, ef_global=eg)
+        np.testing.assert_allclose(a["recon"], b["recon"].T, atol=1e-13)
+        for w in range(D):
+            np.testing.assert_allclose(a["err"][w], b["err"][w].T, atol=1e-13)
+        np.testing.assert_allclose(a["Q"], b["Q"], atol=1e-13)
+        assert a["P_hat"].shape == (m, r)
+
+
+def test_embed_sync_hand_values():
+    """Reading C12: sum over the 2D ranks of G/D = mean(first) + mean(last).
+    Ones on 2D = 8 ranks with D = 4 give 2 (a 1/(2D) scale would give 1); a
+    D = 2 example with distinct values: mean(1,3) + mean(5,7) = 2 + 6 = 8."""
+    D = 4
+    ones = [np.ones((2, 3))] * (2 * D)
+    np.testing.assert_array_equal(oracle.embed_sync_fused(ones, D), 2 * np.ones((2, 3)))
+    np.testing.assert_array_equal(oracle.embed_sync_sequential(ones[:D], ones[D:]), 2 * np.ones((2, 3)))
+    vals = [np.full((1, 2), v) for v in (1.0, 3.0, 5.0, 7.0)]
+    np.testing.assert_array_equal(oracle.embed_sync_fused(vals, 2), np.full((1, 2), 8.0))
+    np.testing.assert_array_equal(oracle.embed_sync_sequential(vals[:2], vals[2:]), np.full((1, 2), 8.0))

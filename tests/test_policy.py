@@ -45,3 +45,12 @@ def test_groups_two_pp_four_dp():
     assert pol.fe_scale(4) == 0.25
     assert pol.is_embedding("language_model.embedding.word_embeddings.weight")
     assert not pol.is_embedding("layers.0.mlp.dense_h_to_4h.weight")
+
+
+def test_kernel_rank_maps_paper_ranks_to_built_instances():
+    p = pol.Policy()
+    assert p.kernel_rank(p.cb_rank) == 16          # PAPER.md:773 CB rank is built
+    assert p.kernel_rank(p.dp_rank) == 64          # 128 is not built: the largest built rank below it
+    assert p.kernel_rank(33) == 32 and p.kernel_rank(4) == 4
+    with pytest.raises(ValueError):
+        p.kernel_rank(3)
