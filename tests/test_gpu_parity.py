@@ -60,12 +60,13 @@ def elem(a, b, ref):
     return np.abs(a - b).max() / max(np.abs(ref).max(), 1e-300)
 
 
-def check_step(g, o, A, *, tol, check_factors=True):
+def check_step(g, o, A, *, tol, check_factors=True, etol=None):
     """Frobenius bound `tol` (north_star) and an element-wise bound relative to
     max |A| on M' and e_new: fp32 1e-5 (tol / 10); bf16 1e-2, since an fp32-
     vs-fp64 difference may flip one bf16 rounding of the largest element, one
     ulp = up to 2^-7 of it; orthonormality; factors column-wise."""
-    etol = tol / 10 if tol <= TOL32 else tol
+    if etol is None:
+        etol = tol / 10 if tol <= TOL32 else tol
     r = g["P_hat"].shape[1]
     orth = np.linalg.norm(g["P_hat"].T @ g["P_hat"] - np.eye(r))
     assert orth <= TOLORTH, orth
@@ -177,7 +178,10 @@ def test_amp_gate_rejects_collinear_factor():
     g = run_gpu(M, e, Q0, r)
     assert g["stats"]["q_fused"] == 0 and g["stats"]["q_amp"] > 32
     o = oracle.compress_step(M, e, Q0)
-    check_step(g, o, M.astype(np.float64) + e, tol=TOL32, check_factors=False)
+    # P is ill conditioned by construction (kappa ~ 1e3-1e4): rounding of the
+    # fp32 factors is amplified by kappa, so the element-wise bound is the
+    # Frobenius one (1e-4 of max |A|) here
+    check_step(g, o, M.astype(np.float64) + e, tol=TOL32, check_factors=False, etol=TOL32)
 
 
 @pytest.mark.parametrize("bf16", [False, True])
