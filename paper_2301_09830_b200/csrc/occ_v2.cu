@@ -531,7 +531,6 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
   // 32 keeps it well inside the 1e-4 parity budget.  Debug bit 2 forces the
   // general path.
   p.amp_thr = (p.debug & 4) ? -1.0 : 32.0;
-  p.spec = (pl.cells_per_warp <= TMEM_CELLS && !(p.debug & 16)) ? 1 : 0;
   p.check_finite = p1.check_finite;
   p.wire_bf16 = p1.wire_bf16;
   auto kern = occ_v2_kernel<R, MBF>;

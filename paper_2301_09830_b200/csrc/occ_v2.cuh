@@ -38,6 +38,8 @@
 #pragma once
 #include "occ_kernels.cuh"
 
+#include <type_traits>
+
 namespace occ {
 namespace v2 {
 
@@ -77,7 +79,6 @@ struct Params2 {
   double amp_thr;      // fused-Q gate on ||S Li^T||_F (phase 3)
   int check_finite;    // OCC_CHECK_FINITE (phase 3)
   int wire_bf16;       // OCC_WIRE_BF16: P_hat rows and the Q slice rounded to bf16 before phase 5
-  int spec;            // every cell TMEM-resident: the fused result is checked after phase 5
   int force_two_pass;
   int debug;           // bit 0: skip phase-1 compute (streaming floor measurement only)
 };
@@ -156,6 +157,26 @@ __device__ __forceinline__ unsigned tf32_rna(float x) {
 __device__ __forceinline__ void split3(float x, unsigned& hi, unsigned& lo) {
   hi = __float_as_uint(x) & 0xffffe000u;
   lo = __float_as_uint(x - __uint_as_float(hi));
+}
+// a + b on a float pair in one FADD2 (sm_100 packed fp32)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long x, y, d;
+  memcpy(&x, &a, 8);
+  memcpy(&y, &b, 8);
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+  float2 r;
+  memcpy(&r, &d, 8);
+  return r;
+}
+// a - b on a float pair in one FADD2
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long x, y, d;
+  memcpy(&x, &a, 8);
+  memcpy(&y, &b, 8);
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+  float2 r;
+  memcpy(&r, &d, 8);
+  return r;
 }
 __device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
   asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"

@@ -56,6 +56,12 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  {   // the staging ring starts zeroed: rows a partial last stage does not copy and the row padding are
+      // read (multiplied by zero factors), so they must hold finite values, never stale NaN bit patterns
+    uint4* z = reinterpret_cast<uint4*>(sm + p.off_stm);
+    const int nz = (p.off_qs - p.off_stm) / 16;
+    for (int x = tid; x < nz; x += NT) z[x] = make_uint4(0u, 0u, 0u, 0u);
+  }
   if (tid == 0) {
     for (int s = 0; s < MAX_STAGES; s++) {
       mbar_init(&mbar[s], 1);                      // full: the producer's expect_tx arrival
@@ -149,92 +155,111 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       }
     }
     if (stamp) p.stats->t_ns[7] = gtimer();
-    const bool has_e = p.err_in != nullptr;
-    for (int s = 0; s < nst; s++) {
-      const int slot = s % p.ns;
-      const unsigned long long tw0 = stamp ? gtimer() : 0;
-      mbar_wait(&full[slot], (unsigned)((s / p.ns) & 1));
-      if (stamp) wait_ns += gtimer() - tw0;
-      const int nrow = min(SR, T.th - s * SR);
-      if (kTrace && (p.debug & 1)) {   // streaming-floor experiment: consume the slot without computing
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        continue;
+    // One stage = SR rows.  Per lane, everything that does not change from stage
+    // to stage is computed once: the staging offsets of its k-step B operands
+    // (row g, columns 8 kk + 2t; a k-step past the tile reads column 2t, finite
+    // data times the zero Q fragment, so the loop has no per-k-step branch) and
+    // of its TMEM cells (rows t, t+4, columns 16 cg + 2g).  Rows past a partial
+    // last stage are not masked: they hold finite staging data (the ring starts
+    // zeroed) and only ever meet zero P rows or bounds-checked stores.  The
+    // slot / parity counters replace a division per stage.
+    auto consume = [&](auto he) {
+      constexpr bool HASE = decltype(he)::value;
+      constexpr int MS = MBF ? 2 : 1;   // M staging: element units per float of the row stride
+      int offB[KREG];   // column of the k-step B operand (row g)
+#pragma unroll
+      for (int j = 0; j < KREG; j++) {
+        const int kk = w + NCW * j;
+        offB[j] = (kk < nk ? 8 * kk : 0) + 2 * t;
       }
-      const unsigned char* sMb = stM + (size_t)slot * SR * sw * 4;
-      const float* sEb = stE + (size_t)slot * SR * sw;
-      // A[i][j..j+1] = M + e (two elements; rows >= nrow read as 0).  No CTA-wide
-      // sync per stage: every warp reads exactly the elements it consumes.
-      auto A2 = [&](int i, int j) -> float2 {
-        float2 a;
-        if (MBF) {
-          a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sMb + ((size_t)i * sw * 4 + (size_t)j * 2)));
+      const int ncw = T.ncg > w ? (T.ncg - w + NCW - 1) / NCW : 0;   // TMEM column groups of this warp
+      const int colC = 16 * w + 2 * g;                                // its first cell's column
+      int slot = 0;
+      unsigned par = 0;
+      for (int s = 0; s < nst; s++) {
+        const unsigned long long tw0 = stamp ? gtimer() : 0;
+        mbar_wait(&full[slot], par);
+        if (stamp) wait_ns += gtimer() - tw0;
+        if (kTrace && (p.debug & 1)) {   // streaming-floor experiment: consume the slot without computing
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
+          if (++slot == p.ns) { slot = 0; par ^= 1u; }
+          continue;
+        }
+        const unsigned char* sMb = stM + (size_t)slot * SR * sw * 4;
+        const float* sEb = stE + (size_t)slot * SR * sw;
+        // A[i][j..j+1] = M + e (FADD2); M rows are sw floats = MS sw elements apart
+        auto A2 = [&](int i, int j) -> float2 {
+          float2 a;
+          if (MBF) a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(
+                       reinterpret_cast<const __nv_bfloat16*>(sMb) + (i * MS * sw + j)));
+          else a = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(sMb) + (i * sw + j));
+          if (HASE) a = add2(a, *reinterpret_cast<const float2*>(sEb + (i * sw + j)));
+          return a;
+        };
+        // (a) P^T[k][rows] = Q_prev^T[k][cols] A^T[cols][rows]; warps split the column k-steps,
+        //     one accumulator chain per k-step (independent MMA chains)
+        float acc[KREG][MT][4];
+#pragma unroll
+        for (int j = 0; j < KREG; j++)
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++) acc[j][mt][0] = acc[j][mt][1] = acc[j][mt][2] = acc[j][mt][3] = 0.f;
+        if constexpr (QREG) {
+          unsigned bh[KREG][2], bl[KREG][2];
+#pragma unroll
+          for (int j = 0; j < KREG; j++) {
+            const float2 b = A2(g, offB[j]);
+            split3(b.x, bh[j][0], bl[j][0]);
+            split3(b.y, bh[j][1], bl[j][1]);
+          }
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+            for (int j = 0; j < KREG; j++) {   // the KREG chains interleave
+              const unsigned ah[4] = {qf[j][mt][0], qf[j][mt][1], qf[j][mt][2], qf[j][mt][3]};
+              mma_tf32(acc[j][mt], ah, bl[j][0], bl[j][1]);
+            }
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+            for (int j = 0; j < KREG; j++) {
+              const unsigned al[4] = {qf[j][mt][4], qf[j][mt][5], qf[j][mt][6], qf[j][mt][7]};
+              mma_tf32(acc[j][mt], al, bh[j][0], bh[j][1]);
+            }
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+            for (int j = 0; j < KREG; j++) {
+              const unsigned ah[4] = {qf[j][mt][0], qf[j][mt][1], qf[j][mt][2], qf[j][mt][3]};
+              mma_tf32(acc[j][mt], ah, bh[j][0], bh[j][1]);
+            }
         } else {
-          a = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(sMb) + (size_t)i * sw + j);
-        }
-        if (has_e) {
-          const float2 e = *reinterpret_cast<const float2*>(sEb + (size_t)i * sw + j);
-          a.x += e.x; a.y += e.y;
-        }
-        return i < nrow ? a : make_float2(0.f, 0.f);
-      };
-      // (a) P^T[k][rows] = Q_prev^T[k][cols] A^T[cols][rows]; warps split the column k-steps,
-      //     one accumulator chain per k-step (independent MMA chains)
-      float acc[KREG][MT][4];
-#pragma unroll
-      for (int j = 0; j < KREG; j++)
-#pragma unroll
-        for (int mt = 0; mt < MT; mt++) acc[j][mt][0] = acc[j][mt][1] = acc[j][mt][2] = acc[j][mt][3] = 0.f;
-      const bool x_mma = kTrace && (p.debug & 128);    // ablation experiments (trace build only)
-      const bool x_tmem = kTrace && (p.debug & 256);
-      const bool x_red = kTrace && (p.debug & 512);
-      if (x_mma) {
-      } else if constexpr (QREG) {
-#pragma unroll
-        for (int j = 0; j < KREG; j++) {
-          const int kk = w + NCW * j;
-          if (kk < nk) {
+          for (int kk = w; kk < nk; kk += NCW) {
             const float2 b = A2(g, 8 * kk + 2 * t);
             unsigned bh0, bl0, bh1, bl1;
             split3(b.x, bh0, bl0);
             split3(b.y, bh1, bl1);
 #pragma unroll
             for (int mt = 0; mt < MT; mt++) {
-              const unsigned ah[4] = {qf[j][mt][0], qf[j][mt][1], qf[j][mt][2], qf[j][mt][3]};
-              const unsigned al[4] = {qf[j][mt][4], qf[j][mt][5], qf[j][mt][6], qf[j][mt][7]};
-              mma3(acc[j][mt], ah, al, bh0, bh1, bl0, bl1);
+              unsigned f[8];
+              qfrag(qs, RP, 8 * kk, mt, f);
+              const unsigned ah[4] = {f[0], f[1], f[2], f[3]}, al[4] = {f[4], f[5], f[6], f[7]};
+              mma3(acc[0][mt], ah, al, bh0, bh1, bl0, bl1);
             }
           }
         }
-      } else {
-        for (int kk = w; kk < nk; kk += NCW) {
-          const float2 b = A2(g, 8 * kk + 2 * t);
-          unsigned bh0, bl0, bh1, bl1;
-          split3(b.x, bh0, bl0);
-          split3(b.y, bh1, bl1);
-#pragma unroll
-          for (int mt = 0; mt < MT; mt++) {
-            unsigned f[8];
-            qfrag(qs, RP, 8 * kk, mt, f);
-            const unsigned ah[4] = {f[0], f[1], f[2], f[3]}, al[4] = {f[4], f[5], f[6], f[7]};
-            mma3(acc[0][mt], ah, al, bh0, bh1, bl0, bl1);
-          }
+        // (b) TMEM: the cells of row block s in this warp's column groups
+        for (int jj = 0; jj < ncw; jj++) {
+          const int cs = jj * T.nrblk + s;   // cell_slot(s, w + NCW jj)
+          if (cs >= TMEM_CELLS) break;       // (cs grows with jj)
+          const int c = colC + 16 * NCW * jj;
+          const float2 x0 = A2(t, c), x1 = A2(t + 4, c);
+          tmem_st4(taddr_w + (unsigned)(cs * 4), x0.x, x1.x, x0.y, x1.y);
         }
-      }
-      // (b) TMEM: cells of row block s in this warp's column groups
-      for (int cg = w; !x_tmem && cg < T.ncg; cg += NCW) {
-        const int cs = cell_slot(s, cg);
-        if (cs >= TMEM_CELLS) continue;
-        const int c = 16 * cg + 2 * g;
-        const bool ok = c < T.tw;   // tw is a multiple of 8, so c + 1 < tw too
-        const float2 x0 = ok ? A2(t, c) : make_float2(0.f, 0.f);
-        const float2 x1 = ok ? A2(t + 4, c) : make_float2(0.f, 0.f);
-        tmem_st4(taddr_w + (unsigned)(cs * 4), x0.x, x1.x, x0.y, x1.y);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);   // this warp is done with the slot
-      if (!x_red) {  // this warp's partial P^T for rows 8s..8s+7 -> its own slot (reduced once after the loop)
-         // D[k][row]: c0 = (k=16mt+g, row=2t), c1 = (g, 2t+1), c2 = (g+8, 2t), c3 = (g+8, 2t+1)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);   // this warp is done with the slot
+        // this warp's partial P^T for rows 8s..8s+7 -> its own slot (reduced once after the loop)
+        // D[k][row]: c0 = (k=16mt+g, row=2t), c1 = (g, 2t+1), c2 = (g+8, 2t), c3 = (g+8, 2t+1)
         float* rw = red + ((size_t)w * nst + s) * SR * RP;
 #pragma unroll
         for (int mt = 0; mt < MT; mt++) {
@@ -249,8 +274,11 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
             rw[(2 * t + 1) * RP + k0 + 8] = a3;
           }
         }
+        if (++slot == p.ns) { slot = 0; par ^= 1u; }
       }
-    }
+    };
+    if (p.err_in) consume(std::true_type{});
+    else consume(std::false_type{});
     consumer_sync();
     // P_part rows of this tile: sum of the NCW warp partials (fixed order)
     for (int x = tid; x < T.th * R; x += NCW * 32) {
@@ -320,27 +348,17 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (stamp) p.stats->t_ns[2] = gtimer();
 
   // ============================================================== phase 3
-  // G = sum of the nr band partials (all threads).  Then, concurrently:
-  //   warp NW-1:     LDL^T of G with the degenerate-column test, publishing each
-  //                  column of L as it is final; then Li, kappa, amp (off the
-  //                  critical path: checked after phase 5)
-  //   compute warps: reduce this CTA's column slice of Q~ over the nr row bands,
-  //                  then P_hat = D^-1/2 L^-1 P and Q = D^-1/2 L^-1 Q~ row by row,
-  //                  one step behind the factorisation (reading C20)
-  // The fused Q is exact up to rounding; its rounding error is amplified by
-  // amp = ||S Li^T|| (= 1/sigma_min of the column-equilibrated P, ~sqrt(r) for
-  // a warm-started P).  A degenerate column or a forced CholQR2 pass takes the
-  // general path at once; kappa > kappa_thr or amp > amp_thr is checked after
-  // phase 5 when every cell is TMEM-resident (spec; the redo recomputes from
-  // TMEM), else before it.
-  // Warp groups (occ_v2_la.cuh): group A reduces G and hands it to warp NW-1
-  // (named barrier 3: A arrives, NW-1 waits), which factors it (LDL^T, the
-  // degenerate-column test) and forms Li, kappa and amp, publishing progress in
-  // o.prog (R + 1: factored, R + 2: Li ready, -1: degenerate).  Meanwhile all
-  // compute warps reduce the Q~ slice.  Then: P_hat = P Li^T, Q = Q~ Li^T in one
-  // parallel pass (reading C20; the fused Q's rounding is amplified by amp =
-  // ||S Li^T||, ~sqrt(r) for a warm-started P).  A degenerate column, a forced
-  // or needed CholQR2 pass, or amp > amp_thr take the general path.
+  // Warp groups (occ_v2_la.cuh): group A reduces G = sum of the nr band
+  // partials and hands it to warp NW-1 (named barrier 3: A arrives, NW-1
+  // waits), which factors it with the degenerate-column test and forms
+  // Li = D^-1/2 L^-1, kappa and amp (R <= 16: one Gauss-Jordan chain on the
+  // augmented [G | I], ldl_inverse_gj; R = 32: LDL^T then the inverse),
+  // publishing o.prog = R + 2 (or -1: degenerate).  Meanwhile all compute warps
+  // reduce this CTA's column slice of Q~ over the nr row bands.  Then P_hat =
+  // P Li^T and Q = Q~ Li^T in one parallel pass (reading C20; the fused Q's
+  // rounding is amplified by amp = ||S Li^T||, ~sqrt(r) for a warm-started P).
+  // A degenerate column, a forced or needed CholQR2 pass (kappa > kappa_thr),
+  // or amp > amp_thr take the general path (cold_orth_q) before phase 5.
   const int2 qs_cols = active ? q_slice(T, p.nr) : make_int2(0, 0);
   const int nqc = qs_cols.y - qs_cols.x;
   const bool force2 = p.force_two_pass != 0;
@@ -348,11 +366,17 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (w == NW - 1) {
     asm volatile("bar.sync 3, %0;" ::"r"((NWA + 1) * 32) : "memory");
     if (p.check_finite && blockIdx.x == 0 && lane < R && !isfinite(o.gdiag[lane])) atomicOr(&g_nonfinite_v2, 1u);
-    deg = ldl_warp_unrolled<R>(o, p.tau * p.tau, true) != 0;
-    trw(8);
-    if (!deg) {
-      inverse_warp_unrolled<R>(o);
+    if constexpr (R <= 16) {   // factor and inverse in one elimination chain
+      deg = ldl_inverse_gj<R>(o, p.tau * p.tau) != 0;
+      trw(8);
       trw(15);
+    } else {
+      deg = ldl_warp_unrolled<R>(o, p.tau * p.tau, true) != 0;
+      trw(8);
+      if (!deg) {
+        inverse_warp_unrolled<R>(o);
+        trw(15);
+      }
     }
   } else {
     if (in_group_a(w)) {
@@ -394,7 +418,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
     for (int x = tid; x < nqc * R; x += NCW * 32) qs_out[x] = rb(qs_out[x]);
   }
   tr(12);
-  for (int pass = 0;; pass++) {
+  {   // (the fused / general decision is final here: phase 3 already knows kappa and amp)
     if (w < NCW) {
       // ---------------------------------------------------------- tables, B3 (compute warps)
       SyncCompute()();   // P_hat rows of every compute thread are written
@@ -427,7 +451,8 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       // used by exactly one lane: it is loaded straight from L2 (no staging, no
       // CTA barrier), the next column group's values while this one computes.
       tr(16);
-      if (active) {
+      auto phase5 = [&](auto hr, auto he) {
+        constexpr bool HASR = decltype(hr)::value, HASE = decltype(he)::value;
         auto load_q = [&](int cg, float (&qv)[KS5][4]) {
           const int cl = 16 * cg + 2 * g;
           const bool okA = cg < T.ncg && cl < T.tw, okB = cg < T.ncg && cl + 1 < T.tw;
@@ -441,6 +466,11 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
             qv[ks][3] = (okB && k0 + 4 < R) ? __ldcg(qa_ + R + k0 + 4) : 0.f;
           }
         };
+        // interior groups of four cells (32 rows, both columns of the lane inside)
+        // store through row pointers advanced by 8 rows per cell: no per-cell
+        // index arithmetic or bounds test
+        const int nfull = T.th / 32;   // row-block groups of 4 with all 32 rows inside
+        using RT = typename std::conditional<MBF, __nv_bfloat16, float>::type;
         float qnext[KS5][4];
         load_q(w, qnext);
         for (int cg = w; cg < T.ncg; cg += NCW) {
@@ -450,87 +480,89 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
 #pragma unroll
             for (int q = 0; q < 4; q++) split3(qnext[ks][q], qh[ks][q], ql[ks][q]);
           load_q(cg + NCW, qnext);
+          const int c = 16 * cg + 2 * g;
+          const bool colin = c + 1 < T.tw;
+          RT* rp = HASR ? reinterpret_cast<RT*>(p.recon) + ((size_t)(T.row0 + t) * p.ldr + (T.col0 + c)) : nullptr;
+          float* ep = HASE ? p.err_out + ((size_t)(T.row0 + t) * p.lde_out + (T.col0 + c)) : nullptr;
+          const size_t r4 = 4 * (size_t)p.ldr, e4 = 4 * (size_t)p.lde_out;
           for (int rb0 = 0; rb0 < T.nrblk; rb0 += 4) {
             float v16[16];
             const int cs0 = cell_slot(rb0, cg);
-            const bool batch = cs0 + 4 <= TMEM_CELLS;
-            if (batch) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
+            if (cs0 + 4 <= TMEM_CELLS) tmem_ld16(taddr_w + (unsigned)(cs0 * 4), v16);
             else cells4_slow<MBF>(p, T, taddr_w, rb0, cg, cs0, g, t, v16);
             const bool first = kTrace && cg == w && rb0 == 0;
             if (first) tr(17);
             float mr4[4][4];   // four cells, four independent MMA chains
 #pragma unroll
             for (int jj = 0; jj < 4; jj++) mr4[jj][0] = mr4[jj][1] = mr4[jj][2] = mr4[jj][3] = 0.f;
-            if (!(kTrace && (p.debug & 64))) {   // (debug 64: no phase-5 MMAs, timing experiment)
 #pragma unroll
-              for (int ks = 0; ks < KS5; ks++)
+            for (int ks = 0; ks < KS5; ks++)
 #pragma unroll
-                for (int jj = 0; jj < 4; jj++) {
-                  const int rblk = min(rb0 + jj, T.nrblk - 1);
-                  const uint4 b = pb[(rblk * KS5 + ks) * 32 + lane];
-                  mma3(mr4[jj], qh[ks], ql[ks], b.x, b.y, b.z, b.w);
-                }
-            }
+              for (int jj = 0; jj < 4; jj++) {
+                const int rblk = min(rb0 + jj, T.nrblk - 1);
+                const uint4 b = pb[(rblk * KS5 + ks) * 32 + lane];
+                mma3(mr4[jj], qh[ks], ql[ks], b.x, b.y, b.z, b.w);
+              }
             if (kTrace && first) {
               if (mr4[0][0] == 1.2345e-30f) p.stats->grid = -2;   // keep the MMA results live before the stamp
               tr(18);
             }
+            if (MBF) {
 #pragma unroll
-            for (int jj = 0; jj < 4; jj++) {
-              const int rblk = rb0 + jj;
-              if (rblk >= T.nrblk) break;
-              float* mr = mr4[jj];
-              const float v[4] = {v16[4 * jj], v16[4 * jj + 1], v16[4 * jj + 2], v16[4 * jj + 3]};
-              if (MBF) {
+              for (int jj = 0; jj < 4; jj++)
 #pragma unroll
-                for (int q = 0; q < 4; q++) mr[q] = __bfloat162float(__float2bfloat16_rn(mr[q]));
-              }
-              // mr/v: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
-              const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
-              if (kTrace && (p.debug & 32)) {   // timing experiment: no phase-5 stores
-                if (mr[0] == 1.2345f && v[0] == 5.4321f) p.stats->grid = -1;
-                continue;
-              }
-              if (r + 4 < T.th && c + 1 < T.tw) {   // both rows and both columns inside: 8-byte pair stores
-                const size_t o0 = (size_t)(T.row0 + r) * p.ldr + (T.col0 + c);
-                if (p.recon) {
+                for (int q = 0; q < 4; q++) mr4[jj][q] = __bfloat162float(__float2bfloat16_rn(mr4[jj][q]));
+            }
+            // mr/v: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
+            if (colin && rb0 / 4 < nfull) {
+#pragma unroll
+              for (int jj = 0; jj < 4; jj++) {
+                const float* mr = mr4[jj];
+                const float* v = v16 + 4 * jj;
+                const size_t ro = (size_t)(8 * jj) * p.ldr, eo = (size_t)(8 * jj) * p.lde_out;
+                if (HASR) {
                   if (MBF) {
-                    __nv_bfloat162* d0 = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + o0);
-                    __nv_bfloat162* d1 =
-                        reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + o0 + 4 * p.ldr);
-                    *d0 = __floats2bfloat162_rn(mr[0], mr[2]);
-                    *d1 = __floats2bfloat162_rn(mr[1], mr[3]);
+                    *reinterpret_cast<__nv_bfloat162*>(rp + ro) = __floats2bfloat162_rn(mr[0], mr[2]);
+                    *reinterpret_cast<__nv_bfloat162*>(rp + ro + r4) = __floats2bfloat162_rn(mr[1], mr[3]);
                   } else {
-                    float* d = reinterpret_cast<float*>(p.recon) + o0;
-                    *reinterpret_cast<float2*>(d) = make_float2(mr[0], mr[2]);
-                    *reinterpret_cast<float2*>(d + 4 * p.ldr) = make_float2(mr[1], mr[3]);
+                    *reinterpret_cast<float2*>(rp + ro) = make_float2(mr[0], mr[2]);
+                    *reinterpret_cast<float2*>(rp + ro + r4) = make_float2(mr[1], mr[3]);
                   }
                 }
-                if (p.err_out) {
-                  float* d = p.err_out + (size_t)(T.row0 + r) * p.lde_out + (T.col0 + c);
-                  *reinterpret_cast<float2*>(d) = make_float2(v[0] - mr[0], v[2] - mr[2]);
-                  *reinterpret_cast<float2*>(d + 4 * p.lde_out) = make_float2(v[1] - mr[1], v[3] - mr[3]);
+                if (HASE) {
+                  *reinterpret_cast<float2*>(ep + eo) = sub2(make_float2(v[0], v[2]), make_float2(mr[0], mr[2]));
+                  *reinterpret_cast<float2*>(ep + eo + e4) = sub2(make_float2(v[1], v[3]), make_float2(mr[1], mr[3]));
                 }
-                continue;
               }
-              store_cell_edge<MBF>(p, T, r, c, make_float4(mr[0], mr[1], mr[2], mr[3]),
-                                   make_float4(v[0], v[1], v[2], v[3]));
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 4; jj++) {
+                const int rblk = rb0 + jj;
+                if (rblk >= T.nrblk) break;
+                const float* mr = mr4[jj];
+                store_cell_edge<MBF>(p, T, 8 * rblk + t, c, make_float4(mr[0], mr[1], mr[2], mr[3]),
+                                     make_float4(v16[4 * jj], v16[4 * jj + 1], v16[4 * jj + 2], v16[4 * jj + 3]));
+              }
             }
+            if (HASR) rp += 32 * (size_t)p.ldr;
+            if (HASE) ep += 32 * (size_t)p.lde_out;
             if (first) tr(19);
           }
           if (cg == w) tr(20);
+        }
+      };
+      if (active) {
+        if (p.recon) {
+          if (p.err_out) phase5(std::true_type{}, std::true_type{});
+          else phase5(std::true_type{}, std::false_type{});
+        } else if (p.err_out) {
+          phase5(std::false_type{}, std::true_type{});
         }
       }
       if (stamp) p.stats->t_ns[6] = gtimer();
       tr(11);
     }
-    __syncthreads();   // warp NW-1's conditioning estimates are complete
-    // spec check (uniform over the grid: every CTA holds the same G): on failure
-    // redo the general path from TMEM and run tables / B3 / phase 5 again
-    if (pass > 0 || !fused || !(o.kappa > p.kappa_thr || o.amp > p.amp_thr)) break;
-    nb = cold_orth_q<R, MBF>(p, T, o, ps, ps2, gscr, pa, taddr_w, nb, active, false);
-    phat = ps;
-    fused = false;
+    __syncthreads();
   }
   if (blockIdx.x == 0 && tid == 0) {
     int cnt = 0;
