@@ -178,7 +178,12 @@ occ_status occ_recv_factors(occ_mat out, occ_mat P, occ_mat Q, int r, int peer, 
  * recv_peer and decompresses them into out (occ_decompress).  The sends and
  * receives form ONE NCCL group, so a ring of stages cannot deadlock.
  * send_peer / recv_peer = -1 skip that side (the pipeline ends).  Shapes as
- * occ_send_factors / occ_recv_factors (out is recv_peer's matrix shape). */
+ * occ_send_factors / occ_recv_factors (out is recv_peer's matrix shape).
+ * M.ptr == NULL sends the factors already in P and Q (exchange only, e.g. to
+ * time the link); out.ptr == NULL receives into Prcv / Qrcv without
+ * decompressing.  Neither form takes OCC_WIRE_BF16 (OCC_ERR_UNSUPPORTED).
+ * A stage may name itself as both peers (a ring of one: the NCCL send and
+ * receive still run, matched inside the group). */
 occ_status occ_sendrecv_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, int send_peer,
                                 occ_mat out, occ_mat Prcv, occ_mat Qrcv, int recv_peer, uint32_t flags,
                                 occ_comm pp, void* ws, size_t ws_bytes, cudaStream_t stream);

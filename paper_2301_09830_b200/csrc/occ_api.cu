@@ -614,17 +614,31 @@ occ_status occ_sendrecv_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, in
   if (rcv && (recv_peer >= pp->nranks || (recv_peer == pp->rank && !self_ok)))
     return fail(OCC_ERR_INVALID_ARG, "bad recv_peer %d", recv_peer);
   const bool wire = (flags & OCC_WIRE_BF16) != 0;
+  // M.ptr == NULL: P and Q already hold the factors to send (exchange only);
+  // out.ptr == NULL: receive the factors only (no decompression)
+  const bool compress = snd && M.ptr != nullptr, decompress = rcv && out.ptr != nullptr;
+  if ((!compress && snd && wire) || (!decompress && rcv && wire))
+    return fail(OCC_ERR_UNSUPPORTED, "OCC_WIRE_BF16 needs M and out (the bf16 staging lives in ws / out)");
   // every argument check before anything is enqueued (occ.h conventions)
   occ_status s;
-  if (snd) {
+  if (compress) {
     if ((s = check_step(M, err, Q, P, nullptr, r, flags))) return s;
     if (wire && (s = check_send_stage_bf16(P.rows, Q.rows, r, ws_bytes, M.rows, M.cols))) return s;
+  } else if (snd) {
+    if ((s = check_rank(r, P.rows, Q.rows))) return s;
+    if ((s = check_view(P, "P", P.rows, r, true, true))) return s;
+    if ((s = check_view(Q, "Q", Q.rows, r, true, true))) return s;
   }
-  if (rcv) {
+  if (decompress) {
     const occ_mat sb[4] = {M, err, Q, P};
     if ((s = check_recv_side(out, Prcv, Qrcv, r, flags, sb, snd ? 4 : 0))) return s;
+  } else if (rcv) {
+    if ((s = check_view(Prcv, "Prcv", Prcv.rows, r, true, true))) return s;
+    if ((s = check_view(Qrcv, "Qrcv", Qrcv.rows, r, true, true))) return s;
+    if (overlap(Prcv, Qrcv) || (snd && (overlap(Prcv, P) || overlap(Prcv, Q) || overlap(Qrcv, P) || overlap(Qrcv, Q))))
+      return fail(OCC_ERR_ALIAS, "receive buffers overlap");
   }
-  if (snd) {
+  if (compress) {
     occ_mat none = {nullptr, 0, 0, 0, M.dtype};
     if ((s = occ_compress(M, err, Q, P, none, r, flags, ws, ws_bytes, stream))) return s;
     if (wire && (s = pack_factors_bf16(P, Q, r, ws, M.rows, M.cols, stream))) return s;
@@ -648,7 +662,7 @@ occ_status occ_sendrecv_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, in
     }
   }
   if ((s = group_end(first, "ncclSendRecv(P,Q)"))) return s;
-  if (!rcv) return OCC_OK;
+  if (!decompress) return OCC_OK;
   if (wire && (s = unpack_factors_bf16(out, Prcv, Qrcv, r, stream))) return s;
   const bool ot = (flags & OCC_ORIENT_T) != 0;
   return ot ? occ_decompress(Qrcv, Prcv, out, stream) : occ_decompress(Prcv, Qrcv, out, stream);

@@ -351,9 +351,10 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   // Warp groups (occ_v2_la.cuh): group A reduces G = sum of the nr band
   // partials and hands it to warp NW-1 (named barrier 3: A arrives, NW-1
   // waits), which factors it with the degenerate-column test and forms
-  // Li = D^-1/2 L^-1, kappa and amp (R <= 16: one Gauss-Jordan chain on the
-  // augmented [G | I], ldl_inverse_gj; R = 32: LDL^T then the inverse),
-  // publishing o.prog = R + 2 (or -1: degenerate).  Meanwhile all compute warps
+  // Li = D^-1/2 L^-1, kappa and amp (LDL^T, then the inverse), publishing
+  // o.prog = R + 2 (or -1: degenerate).  (A single Gauss-Jordan chain on the
+  // augmented [G | I] was tried: its longer straight-line code, fetched cold,
+  // made it slower, 4.6 vs 3.8 us from G to Li.)  Meanwhile all compute warps
   // reduce this CTA's column slice of Q~ over the nr row bands.  Then P_hat =
   // P Li^T and Q = Q~ Li^T in one parallel pass (reading C20; the fused Q's
   // rounding is amplified by amp = ||S Li^T||, ~sqrt(r) for a warm-started P).
@@ -366,17 +367,11 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (w == NW - 1) {
     asm volatile("bar.sync 3, %0;" ::"r"((NWA + 1) * 32) : "memory");
     if (p.check_finite && blockIdx.x == 0 && lane < R && !isfinite(o.gdiag[lane])) atomicOr(&g_nonfinite_v2, 1u);
-    if constexpr (R <= 16) {   // factor and inverse in one elimination chain
-      deg = ldl_inverse_gj<R>(o, p.tau * p.tau) != 0;
-      trw(8);
+    deg = ldl_warp_unrolled<R>(o, p.tau * p.tau, true) != 0;
+    trw(8);
+    if (!deg) {
+      inverse_warp_unrolled<R>(o);
       trw(15);
-    } else {
-      deg = ldl_warp_unrolled<R>(o, p.tau * p.tau, true) != 0;
-      trw(8);
-      if (!deg) {
-        inverse_warp_unrolled<R>(o);
-        trw(15);
-      }
     }
   } else {
     if (in_group_a(w)) {
@@ -466,10 +461,9 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
             qv[ks][3] = (okB && k0 + 4 < R) ? __ldcg(qa_ + R + k0 + 4) : 0.f;
           }
         };
-        // interior groups of four cells (32 rows, both columns of the lane inside)
-        // store through row pointers advanced by 8 rows per cell: no per-cell
-        // index arithmetic or bounds test
-        const int nfull = T.th / 32;   // row-block groups of 4 with all 32 rows inside
+        // cells with all 8 rows and both columns of the lane inside store through
+        // row pointers (advanced by 32 rows per group of four cells): no per-cell
+        // index arithmetic beyond one bounds test
         using RT = typename std::conditional<MBF, __nv_bfloat16, float>::type;
         float qnext[KS5][4];
         load_q(w, qnext);
@@ -514,11 +508,13 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
                 for (int q = 0; q < 4; q++) mr4[jj][q] = __bfloat162float(__float2bfloat16_rn(mr4[jj][q]));
             }
             // mr/v: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
-            if (colin && rb0 / 4 < nfull) {
 #pragma unroll
-              for (int jj = 0; jj < 4; jj++) {
-                const float* mr = mr4[jj];
-                const float* v = v16 + 4 * jj;
+            for (int jj = 0; jj < 4; jj++) {
+              const int rblk = rb0 + jj;
+              if (rblk >= T.nrblk) break;
+              const float* mr = mr4[jj];
+              const float* v = v16 + 4 * jj;
+              if (colin && 8 * rblk + 8 <= T.th) {   // the cell's 8 rows and both columns inside: pair stores
                 const size_t ro = (size_t)(8 * jj) * p.ldr, eo = (size_t)(8 * jj) * p.lde_out;
                 if (HASR) {
                   if (MBF) {
@@ -533,15 +529,9 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
                   *reinterpret_cast<float2*>(ep + eo) = sub2(make_float2(v[0], v[2]), make_float2(mr[0], mr[2]));
                   *reinterpret_cast<float2*>(ep + eo + e4) = sub2(make_float2(v[1], v[3]), make_float2(mr[1], mr[3]));
                 }
-              }
-            } else {
-#pragma unroll
-              for (int jj = 0; jj < 4; jj++) {
-                const int rblk = rb0 + jj;
-                if (rblk >= T.nrblk) break;
-                const float* mr = mr4[jj];
+              } else {
                 store_cell_edge<MBF>(p, T, 8 * rblk + t, c, make_float4(mr[0], mr[1], mr[2], mr[3]),
-                                     make_float4(v16[4 * jj], v16[4 * jj + 1], v16[4 * jj + 2], v16[4 * jj + 3]));
+                                     make_float4(v[0], v[1], v[2], v[3]));
               }
             }
             if (HASR) rp += 32 * (size_t)p.ldr;

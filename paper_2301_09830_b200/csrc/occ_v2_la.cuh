@@ -325,103 +325,6 @@ __device__ void inverse_warp_unrolled(OrthW& o) {
   if (c == 0) prog_release(o, R + 2);
 }
 
-// Factorisation and explicit inverse in ONE elimination (R <= 16): the warp
-// holds the augmented [G | I], lane c < R column c of G, lane R + c column c of
-// I.  Step j eliminates below the pivot d_j = G'_jj with unit multipliers:
-// column x: a_x[i] -= a_j[i] (a_x[j] / d_j), i > j.  After R steps the left
-// half is D L^T and the right half L^-1 (G = L D L^T), so Li = D^-1/2 L^-1 comes
-// out of the same 16-step chain instead of an LDL chain followed by a
-// forward-substitution chain.  The pivot column a_j is broadcast through
-// shared memory before d_j's reciprocal is needed, so a step's critical path
-// is one reciprocal, one multiply and one FMA.  Same degenerate-column test,
-// publish protocol (o.prog = R + 2 when Li, kappa and amp are ready; -1 when a
-// column is degenerate), and outputs (o.Li, o.L, o.D, o.dinv, kappa, amp) as
-// ldl_warp_unrolled + inverse_warp_unrolled; the arithmetic order differs
-// (rounding level), both are fp64.
-template <int R>
-__device__ int ldl_inverse_gj(OrthW& o, double tau2) {
-  static_assert(R <= 16, "the augmented matrix needs 2R <= 32 lanes");
-  const int x = threadIdx.x & 31;
-  const bool gl = x < R, il = x >= R && x < 2 * R;   // G column / identity column lanes
-  const int c = gl ? x : x - R;
-  double a[R];
-#pragma unroll
-  for (int i = 0; i < R; i++) a[i] = gl ? o.L[i * LD + c] : ((il && i == c) ? 1.0 : 0.0);
-  double* buf = o.col;   // two R-double halves: column j of step j in half j & 1
-  if (x == 0) {
-#pragma unroll
-    for (int i = 0; i < R; i++) buf[i] = a[i];
-  }
-  __syncwarp();
-  double dpiv[R];
-  int deg = 0;
-#pragma unroll
-  for (int j = 0; j < R; j++) {
-    const double* cj = buf + 16 * (j & 1);
-    double colj[R];
-#pragma unroll
-    for (int i = 0; i < R; i++) colj[i] = (i >= j) ? cj[i] : 0.0;
-    const double d = colj[j];
-    dpiv[j] = d;
-    const double gj = o.gdiag[j];
-    if (gj == 0.0 || !(d >= tau2 * gj)) { deg = 1; break; }
-    const double tx = a[j] * rcp_fast(d);   // this column's multiple of the pivot row
-#pragma unroll
-    for (int i = j + 1; i < R; i++) a[i] = fma(-colj[i], tx, a[i]);
-    if (j + 1 < R && x == j + 1) {
-      double* cn = buf + 16 * ((j + 1) & 1);
-#pragma unroll
-      for (int i = 0; i < R; i++) cn[i] = a[i];
-    }
-    __syncwarp();
-  }
-  if (deg) {
-    if (x == 0) prog_release(o, -1);
-    return 1;
-  }
-  double dinv[R];
-#pragma unroll
-  for (int i = 0; i < R; i++) dinv[i] = 1.0 / sqrt(dpiv[i]);
-  // lane R + c: column c of Li = D^-1/2 L^-1; lane c: column c of D L^T (row c of L scaled)
-  double ni = 0.0, nl = 0.0, na = 0.0;
-  if (il) {
-#pragma unroll
-    for (int i = 0; i < R; i++) {
-      const double v = a[i] * dinv[i];
-      o.Li[i * LD + c] = v;
-      ni = fma(v, v, ni);
-    }
-    na = o.gdiag[c] * ni;   // ||p_c||^2 ||Li[:, c]||^2
-  }
-  if (gl) {   // ||L D^1/2||_F^2 = sum_{r <= c} (D L^T)[r][c]^2 / d_r
-#pragma unroll
-    for (int i = 0; i < R; i++)
-      if (i <= c) nl = fma(a[i] * a[i], dinv[i] * dinv[i], nl);
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    nl += __shfl_xor_sync(0xffffffffu, nl, off);
-    ni += __shfl_xor_sync(0xffffffffu, ni, off);
-    na += __shfl_xor_sync(0xffffffffu, na, off);
-  }
-  if (x == 0) {
-    o.kappa = sqrt(nl) * sqrt(ni);
-    o.amp = sqrt(na);
-  }
-  __syncwarp();
-  if (x == 0) prog_release(o, R + 2);
-  // the unit lower L (cold paths only): L[r][c] = (D L^T)[c][r] / d_c, written by
-  // lane r from its column of D L^T; D and D^-1/2
-  if (gl) {
-#pragma unroll
-    for (int k = 0; k < R; k++) o.L[c * LD + k] = (k < c) ? a[k] / dpiv[k] : (k == c ? 1.0 : 0.0);
-    o.D[c] = dpiv[c];
-    o.dinv[c] = dinv[c];
-  }
-  __syncwarp();
-  return 0;
-}
-
 // Fused path (reading C20): rows -> D^-1/2 L^-1 rows = rows Li^T with the
 // explicit Li, for the H8 rows of the P band (rows >= th zero; -> P_hat) and
 // the nqc rows of the reduced Q~ slice (-> Q).  4 threads per row, each forming

@@ -192,10 +192,12 @@ def occ_recv_factors(out, P, Q, r: int, peer: int, comm: "Comm", flags: int = 0,
 def occ_sendrecv_factors(M, err, Q, P, r: int, send_peer: int, out, Prcv, Qrcv, recv_peer: int, comm: "Comm",
                          flags: int = 0, ws=None, stream=None):
     """PP steady state: compress M and send (P, Q) to send_peer while receiving
-    recv_peer's factors and decompressing them into out (one NCCL group)."""
-    if send_peer >= 0 and ws is None:
+    recv_peer's factors and decompressing them into out (one NCCL group).
+    M None: send P, Q as they are; out None: receive without decompressing."""
+    if send_peer >= 0 and ws is None and M is not None:
         ws = alloc_workspace(M.shape[0], M.shape[1], r, device=M.device)
-    _check(lib().occ_sendrecv_factors(mat(M) if send_peer >= 0 else mat(None), mat(err), mat(Q), mat(P), r, send_peer,
+    _check(lib().occ_sendrecv_factors(mat(M) if send_peer >= 0 and M is not None else mat(None), mat(err), mat(Q),
+                                      mat(P), r, send_peer,
                                       mat(out), mat(Prcv), mat(Qrcv), recv_peer, flags, comm.handle,
                                       ws.data_ptr() if ws is not None else None,
                                       ws.numel() if ws is not None else 0, _stream(stream)), "occ_sendrecv_factors")

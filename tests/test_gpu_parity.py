@@ -535,3 +535,20 @@ def test_single_rank_embed_sync_dense():
             assert torch.equal(G, to_dev(G0) * sc)
     finally:
         comm.destroy()
+
+
+def test_single_rank_exchange_only():
+    """occ_sendrecv_factors with M = NULL and out = NULL: the library's factor
+    exchange alone (what bench.py times as factor comm), here to self on a
+    1-rank communicator; the received factors equal the sent ones bit for bit."""
+    n, m, r = 1024, 3072, 16
+    comm = occ.Comm.single()
+    try:
+        P = to_dev(synth.q0(n, r, 151))
+        Q = to_dev(synth.q0(m, r, 152))
+        Pr, Qr = torch.empty_like(P), torch.empty_like(Q)
+        occ.occ_sendrecv_factors(None, None, Q, P, r, 0, None, Pr, Qr, 0, comm)
+        occ.occ_check_status(comm=comm)
+        assert torch.equal(Pr, P) and torch.equal(Qr, Q)
+    finally:
+        comm.destroy()
