@@ -549,6 +549,7 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
     p.dp_local_err = dpl ? 1 : 0;
     p.recon = G[i].ptr;
     p.ldr = G[i].ld;
+    p.f_tc = 1;
     cudaError_t e = run_phases(p, g, 8, 9, multi, dpl, stream);
     if (e != cudaSuccess) return cuda_fail(e, "dp reconstruct launch");
   }

@@ -84,6 +84,7 @@ struct Params {
   int check_finite;      // OCC_CHECK_FINITE: flag a non-finite Gram diagonal (non-finite M or e)
   int wire_bf16;         // OCC_WIRE_BF16: round P_hat and Q to bf16 before the reconstruction
   int path;
+  int f_tc;              // phase F on the tensor cores (occ_tc.cuh phase_F_tc; the DP paths)
 };
 
 // ------------------------------------------------------------------ helpers

@@ -2,6 +2,7 @@
 // The phase bodies live in occ_kernels.cuh (see its header comment).
 #include "occ_kernels.cuh"
 #include "occ_internal.h"
+#include "occ_tc.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -14,7 +15,7 @@ template <int R>
 __host__ __device__ constexpr size_t orth_bytes() { return (sizeof(OrthSmem<R>) + 15) / 16 * 16; }
 
 template <int R, bool DPL>
-__global__ void __launch_bounds__(NT, (R <= 32) ? 2 : 1) occ_step_kernel(Params p, int ph0, int ph1, int coop) {
+__global__ void __launch_bounds__(NT, (R <= 16) ? 2 : 1) occ_step_kernel(Params p, int ph0, int ph1, int coop) {
   extern __shared__ __align__(16) unsigned char smraw[];
   float* sm = reinterpret_cast<float*>(smraw);
   unsigned nb = 0;
@@ -23,7 +24,10 @@ __global__ void __launch_bounds__(NT, (R <= 32) ? 2 : 1) occ_step_kernel(Params 
   if (stamp) p.stats->t_ns[0] = gtimer();
   for (int ph = ph0; ph < ph1; ph++) {
     switch (ph) {
-      case P_A: phase_A<R>(p, sm); break;
+      case P_A:   // tensor-core sweep 1 (occ_tc.cuh)
+        if (p.m_bf16) tc::phase_A_tc<R, true>(p, smraw);
+        else tc::phase_A_tc<R, false>(p, smraw);
+        break;
       case P_B1: {
         const bool g = ph1 > P_B2;
         phase_B<R>(p, sm, true, g);
@@ -54,9 +58,19 @@ __global__ void __launch_bounds__(NT, (R <= 32) ? 2 : 1) occ_step_kernel(Params 
         if (__ldcg(p.ctl) == 3) phase_C3<R>(p, o, ps);
         break;
       }
-      case P_D: phase_D<R>(p, sm); break;
+      case P_D:   // tensor-core sweep 2 (occ_tc.cuh)
+        if (p.m_bf16) tc::phase_D_tc<R, true>(p, smraw);
+        else tc::phase_D_tc<R, false>(p, smraw);
+        break;
       case P_E: phase_E<R>(p); break;
-      case P_F: phase_F<R, DPL>(p, sm); break;
+      case P_F:
+        if (p.f_tc && !p.Ploc && !p.Pstate_out) {   // the DP reconstruction (occ_tc.cuh)
+          if (p.m_bf16) tc::phase_F_tc<R, DPL, true>(p, smraw);
+          else tc::phase_F_tc<R, DPL, false>(p, smraw);
+        } else {
+          phase_F<R, DPL>(p, sm);
+        }
+        break;
       default: break;
     }
     if (ph + 1 < ph1) bar();
@@ -85,11 +99,12 @@ __global__ void __launch_bounds__(NT, (R <= 32) ? 2 : 1) occ_step_kernel(Params 
 // ------------------------------------------------------------------ sizes
 template <int R>
 static size_t smem_bytes_for(const Geometry& g) {
-  size_t a = ((size_t)g.cs1 * R + 4 * (size_t)Cfg<R>::A_ROWS * R * 32) * 4;
+  size_t a = tc::smem_A_tc<R>(g.cs1);
   size_t b = (size_t)B_ROWS * R * 4;
   size_t c = orth_bytes<R>() + 2 * (size_t)B_ROWS * R * 4;
-  size_t d = ((size_t)g.rs2 * R + 4 * (size_t)Cfg<R>::CPT * Cfg<R>::KS * 32) * 4;
-  size_t f = 2 * (size_t)F_ROWS * R * 4;   // P rows + Ploc rows (DP, OCC_ORIENT_T)
+  size_t d = tc::smem_D_tc<R>(g.rs2);
+  size_t f = std::max(2 * (size_t)F_ROWS * R * 4,   // P rows + Ploc rows (DP, OCC_ORIENT_T)
+                      tc::smem_F_tc<R>());
   return std::max({a, b, c, d, f});
 }
 
@@ -116,7 +131,7 @@ Geometry make_geometry(int64_t n, int64_t m, int r, int sms) {
   cs1 = std::min<int64_t>(cs1, (m + 7) / 8 * 8);
   g.cs1 = (int)cs1;
   g.s1 = (int)((m + cs1 - 1) / cs1);
-  g.rs2 = 128;
+  g.rs2 = 256;   // rows per sweep-2 split: Q_part holds s2 = n / 256 partials
   g.s2 = (int)((n + g.rs2 - 1) / g.rs2);
   g.ngp = (int)((n + B_ROWS - 1) / B_ROWS);
   return g;
@@ -209,11 +224,13 @@ static cudaError_t run_t(Params p, const Geometry& g, int ph0, int ph1, bool mul
   auto units = [&](int ph) -> int {
     const int64_t n = g.n, m = g.m;
     switch (ph) {
-      case P_A: return (int)(((n + Cfg<R>::A_UR - 1) / Cfg<R>::A_UR) * g.s1);
+      case P_A: return (int)(((n + tc::TcCfg<R>::A_ROWS - 1) / tc::TcCfg<R>::A_ROWS) * g.s1);
       case P_B1: case P_B2: case P_C1: case P_C2: case P_C3: return g.ngp;
-      case P_D: return (int)(((m + Cfg<R>::D_CB - 1) / Cfg<R>::D_CB) * g.s2);
+      case P_D: return (int)(((m + tc::TcCfg<R>::D_COLS - 1) / tc::TcCfg<R>::D_COLS) * g.s2);
       case P_E: return (int)((m + 31) / 32);
-      case P_F: return (int)(((m + CfgF<R, DPL>::CB - 1) / CfgF<R, DPL>::CB) * ((n + F_ROWS - 1) / F_ROWS));
+      case P_F:
+        if (p.f_tc) return (int)(((m + tc::F_TC_COLS - 1) / tc::F_TC_COLS) * ((n + tc::F_TC_ROWS - 1) / tc::F_TC_ROWS));
+        return (int)(((m + CfgF<R, DPL>::CB - 1) / CfgF<R, DPL>::CB) * ((n + F_ROWS - 1) / F_ROWS));
     }
     return 1;
   };

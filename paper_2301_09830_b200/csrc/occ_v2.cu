@@ -250,21 +250,23 @@ struct DecArgs {
   long long lde_out;
 };
 
-// row blocks per work item: 8, or 4 at r = 64 (the prefetched P fragment is RBI x r/8 x 2 registers)
-__host__ __device__ constexpr int dec_rbi(int r) { return r <= 32 ? 8 : 4; }
+// row blocks per work item: 8, or 4 at r = 64 (the prefetched P fragment is RBI x r/8 x 2 registers);
+// with EF the next item's M and e are prefetched too (4 x RBI registers each), so fewer
+__host__ __device__ constexpr int dec_rbi(int r, bool ef) { return ef ? (r <= 16 ? 4 : 2) : (r <= 32 ? 8 : 4); }
 
 template <int R, bool BF, bool EF>
 __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs d) {
   const float* __restrict__ P = d.P;
   const float* __restrict__ Q = d.Q;
   const int n = d.n, m = d.m;
-  constexpr int KS5 = K<R>::KS5, RBI = dec_rbi(R);
+  constexpr int KS5 = K<R>::KS5, RBI = dec_rbi(R, EF);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int ncg = (m + 15) / 16, nrb = (n + 7) / 8;
   const int nitems = ncg * ((nrb + RBI - 1) / RBI);
   // operands of one work item (a 16-column group x RBI row blocks), fetched one
   // item ahead so the L2 latency overlaps the previous item's MMAs and stores
-  auto fetch = [&](int item, float (&qv)[KS5][4], float (&pf)[RBI][KS5][2]) {
+  constexpr int RBE = EF ? RBI : 1;
+  auto fetch = [&](int item, float (&qv)[KS5][4], float (&pf)[RBI][KS5][2], float2 (&am)[RBE][2], float2 (&ae)[RBE][2]) {
     const bool ok = item < nitems;
     const int cg = ok ? item % ncg : 0, rb0 = ok ? (item / ncg) * RBI : nrb;
     const int cl = 16 * cg + 2 * g;   // A operand Q (M = columns 2g | 2g+1, K = rank), as in phase 5
@@ -288,11 +290,33 @@ __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs
         pf[j][ks][1] = (rn < n && k + 4 < R) ? __ldg(P + (size_t)rn * R + k + 4) : 0.f;
       }
     }
+    if constexpr (EF) {   // the item's M and e (rows 8 rblk + t + 4h, columns c, c + 1): in flight one item ahead
+      const int c = 16 * cg + 2 * g;
+#pragma unroll
+      for (int j = 0; j < RBI; j++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int row = 8 * (rb0 + j) + t + 4 * h;
+          const bool in = ok && row < n && c < m;   // m % 8 == 0: c + 1 < m too
+          am[j][h] = make_float2(0.f, 0.f);
+          ae[j][h] = make_float2(0.f, 0.f);
+          if (in) {
+            if (d.m_bf16) {
+              am[j][h].x = __uint_as_float(__ldcs(reinterpret_cast<const unsigned*>(
+                  reinterpret_cast<const __nv_bfloat16*>(d.M) + (size_t)row * d.ldm + c)));
+            } else {
+              am[j][h] = __ldcs(reinterpret_cast<const float2*>(reinterpret_cast<const float*>(d.M) + (size_t)row * d.ldm + c));
+            }
+            if (d.err_in) ae[j][h] = *reinterpret_cast<const float2*>(d.err_in + (size_t)row * d.lde_in + c);
+          }
+        }
+    }
   };
   const int stride = gridDim.x * 8;
   int item = blockIdx.x * 8 + warp;
   float qv[KS5][4], pf[RBI][KS5][2];
-  fetch(item, qv, pf);
+  float2 am[RBE][2], ae[RBE][2];
+  fetch(item, qv, pf, am, ae);
   for (; item < nitems; item += stride) {
     const int cg = item % ncg, rb0 = (item / ncg) * RBI;
     unsigned qh[KS5][4], ql[KS5][4];
@@ -312,7 +336,12 @@ __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs
         mma3(mrs[j], qh[ks], ql[ks], h0, h1, l0, l1);
       }
     }
-    fetch(item + stride, qv, pf);   // next item's operands, in flight during the stores
+    float2 cm[RBE][2], ce[RBE][2];   // this item's M and e (EF)
+#pragma unroll
+    for (int j = 0; j < RBE; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) { cm[j][h] = am[j][h]; ce[j][h] = ae[j][h]; }
+    fetch(item + stride, qv, pf, am, ae);   // next item's operands, in flight during the stores
 #pragma unroll
     for (int j = 0; j < RBI; j++) {
       const int rblk = rb0 + j;
@@ -329,36 +358,17 @@ __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs
           v0 = __bfloat162float(__float2bfloat16_rn(v0));
           v1 = __bfloat162float(__float2bfloat16_rn(v1));
         }
-        // EF: A = M + e_old is loaded BEFORE M' is stored, so recon may alias M
-        // (an in-place occ_compress) and err_out may alias err_in
+        // EF: A = M + e_old was loaded with the item's operands, BEFORE any M' of
+        // the item is stored, so recon may alias M and err_out may alias err_in
         float a0 = 0.f, a1 = 0.f;
         if constexpr (EF) {
+          float2 mv = cm[j][h];
           if (d.m_bf16) {
-            const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(d.M) + (size_t)row * d.ldm + c;
-            if (two) {
-              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(src));
-              a0 = f.x; a1 = f.y;
-            } else {
-              a0 = __bfloat162float(src[0]);
-            }
-          } else {
-            const float* src = reinterpret_cast<const float*>(d.M) + (size_t)row * d.ldm + c;
-            if (two) {
-              const float2 f = __ldcs(reinterpret_cast<const float2*>(src));
-              a0 = f.x; a1 = f.y;
-            } else {
-              a0 = src[0];
-            }
+            const unsigned raw = __float_as_uint(cm[j][h].x);
+            mv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw));
           }
-          if (d.err_in) {
-            const float* src = d.err_in + (size_t)row * d.lde_in + c;
-            if (two) {
-              const float2 f = *reinterpret_cast<const float2*>(src);
-              a0 += f.x; a1 += f.y;
-            } else {
-              a0 += src[0];
-            }
-          }
+          a0 = mv.x + ce[j][h].x;
+          a1 = mv.y + ce[j][h].y;
         }
         if (d.out) {
           const size_t o0 = (size_t)row * d.ldo + c;
@@ -589,7 +599,7 @@ unsigned take_nonfinite_v2() {
 }
 
 static cudaError_t launch_v2_decompress(const v2::DecArgs& d, int r, bool bf16, bool ef, cudaStream_t st) {
-  const int rbi = v2::dec_rbi(r);
+  const int rbi = v2::dec_rbi(r, ef);
   const int items = ((d.m + 15) / 16) * (((d.n + 7) / 8 + rbi - 1) / rbi);
   const int grid = std::max(1, std::min((items + 7) / 8, 148 * 2));   // persistent: 2 CTAs per SM
   switch (r) {
