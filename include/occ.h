@@ -195,6 +195,35 @@ occ_status occ_embed_sync(occ_mat G, occ_mat err, occ_mat Q, occ_mat P, int r, f
                           uint32_t flags, occ_comm emb, void* ws, size_t ws_bytes,
                           cudaStream_t stream);
 
+/* In-kernel factor exchange over NVLink peer memory (
+ * PAPER.md:681-682 §Impl, the P2P low-rank send of compressed
+ * backpropagation, here without a host-issued collective).  A link is this
+ * stage's pair of pipeline neighbours: it sends to send_peer and receives from
+ * recv_peer (ranks of `pp`; -1: none; both may be this rank, a ring of one).
+ * occ_link_open is collective over `pp`: every rank allocates a mailbox of two
+ * slots of (max_rows + max_cols) x r fp32 plus flag words, exports it with
+ * CUDA IPC and maps its neighbours' (handles all-gathered over `pp`).
+ *   sender:   the compression kernel itself writes P_hat and Q into slot
+ *             seq % 2 of send_peer's mailbox with NVLink stores (the fused
+ *             kernel's producer warp does it during phase 5; other paths use
+ *             a push kernel) and releases flag = seq (system scope).
+ *   receiver: the decompression kernel acquires its flag >= seq, decompresses
+ *             straight from the slot, copies the factors to Prcv / Qrcv, and
+ *             acknowledges seq to recv_peer (which reuses the slot two steps
+ *             later).
+ * No NCCL call is on this path.  A wait that exceeds ~2 s (peer gone) aborts
+ * the kernel's wait and occ_check_status reports OCC_ERR_NCCL. */
+typedef struct occ_link_s* occ_link;
+occ_status occ_link_open(occ_comm pp, int send_peer, int recv_peer, int64_t max_rows, int64_t max_cols, int r,
+                         occ_link* out);
+occ_status occ_link_close(occ_link link);
+/* occ_sendrecv_factors over a link (same arguments and semantics, M.ptr == NULL:
+ * push the factors already in P / Q; out.ptr == NULL: receive into Prcv / Qrcv
+ * only).  OCC_WIRE_BF16 is allowed: the factors are bf16-exact fp32 values. */
+occ_status occ_sendrecv_factors_link(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, occ_mat out, occ_mat Prcv,
+                                     occ_mat Qrcv, uint32_t flags, occ_link link, void* ws, size_t ws_bytes,
+                                     cudaStream_t stream);
+
 /* Communicators (NCCL over NVLink / NVSwitch). */
 occ_status occ_get_unique_id(uint8_t id[128]);
 occ_status occ_comm_init(occ_comm* comm, const uint8_t id[128], int nranks, int rank);

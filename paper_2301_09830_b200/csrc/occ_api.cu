@@ -296,6 +296,9 @@ occ_status unpack_factors_bf16(const occ_mat& out, const occ_mat& Prcv, const oc
 
 }  // namespace
 
+static occ_status compress_impl(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat recon, int r, uint32_t flags,
+                                void* ws, size_t ws_bytes, cudaStream_t stream, const LinkPush* push, bool* pushed);
+
 extern "C" {
 
 const char* occ_status_string(occ_status s) {
@@ -338,6 +341,17 @@ occ_status occ_init_q(occ_mat Q, uint64_t seed, cudaStream_t stream) {
 occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat recon, int r, uint32_t flags,
                         void* ws, size_t ws_bytes, cudaStream_t stream) {
   NvtxRange nvtx_("occ_compress");
+  return compress_impl(M, err, Q, P, recon, r, flags, ws, ws_bytes, stream, nullptr, nullptr);
+}
+
+}  // extern "C"
+
+// occ_compress; with `push` (occ_link sender) the fused kernel also pushes the
+// factors to the peer's mailbox (*pushed = true) -- the other paths leave it to
+// the caller (*pushed = false).
+static occ_status compress_impl(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat recon, int r, uint32_t flags,
+                                void* ws, size_t ws_bytes, cudaStream_t stream, const LinkPush* push, bool* pushed) {
+  if (pushed) *pushed = false;
   occ_status s = check_step(M, err, Q, P, &recon, r, flags);
   if (s) return s;
   Geometry g = make_geometry(M.rows, M.cols, r, kGeomSms);
@@ -378,8 +392,13 @@ occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat re
     return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_compress (OCC_ORIENT_T) launch");
   }
   if (!multi && !want_v1() && L.v2_tail_bytes > 0) {
+    if (push) p.push = *push;
     cudaError_t e2 = run_v2(p, r, static_cast<char*>(ws) + L.v2_tail, L.v2_tail_bytes, kGeomSms, stream);
-    if (e2 == cudaSuccess) return OCC_OK;
+    if (e2 == cudaSuccess) {
+      if (pushed) *pushed = push != nullptr;
+      return OCC_OK;
+    }
+    p.push = LinkPush{};
     if (e2 != cudaErrorNotSupported) return cuda_fail(e2, "occ_compress (fused v2) launch");
   }
   cudaError_t e;
@@ -391,6 +410,8 @@ occ_status occ_compress(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, occ_mat re
   if (e == cudaSuccess) e = reconstruct(p, g, r, multi, stream);
   return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_compress launch");
 }
+
+extern "C" {
 
 occ_status occ_decompress(occ_mat P, occ_mat Q, occ_mat out, cudaStream_t stream) {
   NvtxRange nvtx_("occ_decompress");
@@ -777,6 +798,7 @@ occ_status occ_check_status(cudaStream_t stream, occ_comm comm) {
     if (nr != ncclSuccess) return nccl_fail(nr, "ncclCommGetAsyncError");
     if (ar != ncclSuccess) return nccl_fail(ar, "nccl async");
   }
+  if (take_link_timeout()) return fail(OCC_ERR_NCCL, "occ_link: a wait for the peer timed out (peer gone?)");
   const unsigned nf = take_nonfinite_v1() | take_nonfinite_v2();
   if (nf) return fail(OCC_ERR_NONFINITE, "non-finite M or err in a call made with OCC_CHECK_FINITE");
   return OCC_OK;
@@ -807,4 +829,187 @@ extern "C" occ_status occ_read_trace(const void* ws, uint64_t* out, int count, c
   cudaError_t e = cudaMemcpyAsync(out, static_cast<const char*>(ws) + kTraceOffset, words * 8, cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_read_trace");
+}
+
+// ------------------------------------------------------------------ occ_link (f1)
+// Mailbox of one rank: two slots of (max_rows + max_cols) x r fp32, then the
+// words at words_off: +0 flag (released by the rank that sends to us), +64 ack
+// (released by the rank we send to), +128 / +192 our push / receive CTA-exit
+// counters.  The neighbours' mailboxes are mapped with CUDA IPC.
+struct occ_link_s {
+  occ_comm pp = nullptr;
+  int send_peer = -1, recv_peer = -1, r = 0;
+  int64_t cap_rows = 0;        // max_rows + max_cols: P rows + Q rows of one message
+  size_t slot_bytes = 0, words_off = 0;
+  char* local = nullptr;
+  char* send_base = nullptr;   // send_peer's mailbox
+  char* recv_base = nullptr;   // recv_peer's mailbox
+  bool send_ipc = false, recv_ipc = false;
+  unsigned send_seq = 0, recv_seq = 0;
+};
+
+namespace {
+constexpr size_t kLinkFlag = 0, kLinkAck = 64, kLinkPushCtr = 128, kLinkRecvCtr = 192;
+unsigned* link_word(char* base, const occ_link_s* L, size_t off) {
+  return reinterpret_cast<unsigned*>(base + L->words_off + off);
+}
+}  // namespace
+
+extern "C" occ_status occ_link_open(occ_comm pp, int send_peer, int recv_peer, int64_t max_rows, int64_t max_cols,
+                                    int r, occ_link* out) {
+  NvtxRange nvtx_("occ_link_open");
+  if (!pp || !out) return fail(OCC_ERR_INVALID_ARG, "null communicator or output");
+  if (send_peer >= pp->nranks || recv_peer >= pp->nranks || send_peer < -1 || recv_peer < -1)
+    return fail(OCC_ERR_INVALID_ARG, "bad peer (send %d, recv %d, nranks %d)", send_peer, recv_peer, pp->nranks);
+  if (max_rows < 1 || max_cols < 1 || r < 1) return fail(OCC_ERR_SHAPE, "bad link capacity");
+  occ_link L = new occ_link_s;
+  L->pp = pp;
+  L->send_peer = send_peer;
+  L->recv_peer = recv_peer;
+  L->r = r;
+  L->cap_rows = max_rows + max_cols;
+  L->slot_bytes = ((size_t)L->cap_rows * r * 4 + 255) / 256 * 256;
+  L->words_off = 2 * L->slot_bytes;
+  const size_t bytes = L->words_off + 256;
+  auto bail = [&](occ_status st) {
+    if (L->send_ipc) cudaIpcCloseMemHandle(L->send_base);
+    if (L->recv_ipc && L->recv_base != L->send_base) cudaIpcCloseMemHandle(L->recv_base);
+    if (L->local) cudaFree(L->local);
+    delete L;
+    return st;
+  };
+  cudaError_t e = cudaMalloc(&L->local, bytes);
+  if (e == cudaSuccess) e = cudaMemset(L->local, 0, bytes);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "link mailbox"));
+  // all-gather the IPC handles over the communicator
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, L->local);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaIpcGetMemHandle"));
+  const int n = pp->nranks;
+  char* dbuf = nullptr;
+  e = cudaMalloc(&dbuf, (size_t)(n + 1) * sizeof h);
+  if (e == cudaSuccess) e = cudaMemcpy(dbuf + (size_t)n * sizeof h, &h, sizeof h, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (dbuf) cudaFree(dbuf);
+    return bail(cuda_fail(e, "link handle exchange"));
+  }
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  ncclResult_t nr = ncclAllGather(dbuf + (size_t)n * sizeof h, dbuf, sizeof h, ncclUint8, pp->comm, st);
+  e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  std::string hb((size_t)n * sizeof h, '\0');
+  if (nr == ncclSuccess && e == cudaSuccess) e = cudaMemcpy(&hb[0], dbuf, hb.size(), cudaMemcpyDeviceToHost);
+  cudaFree(dbuf);
+  if (nr != ncclSuccess) return bail(nccl_fail(nr, "ncclAllGather(link handles)"));
+  if (e != cudaSuccess) return bail(cuda_fail(e, "link handle exchange"));
+  auto open_peer = [&](int peer, char** base, bool* ipc) -> occ_status {
+    if (peer < 0) return OCC_OK;
+    if (peer == pp->rank) { *base = L->local; return OCC_OK; }
+    cudaIpcMemHandle_t ph;
+    memcpy(&ph, hb.data() + (size_t)peer * sizeof ph, sizeof ph);
+    cudaError_t e2 = cudaIpcOpenMemHandle(reinterpret_cast<void**>(base), ph, cudaIpcMemLazyEnablePeerAccess);
+    if (e2 != cudaSuccess) return cuda_fail(e2, "cudaIpcOpenMemHandle");
+    *ipc = true;
+    return OCC_OK;
+  };
+  occ_status s = open_peer(send_peer, &L->send_base, &L->send_ipc);
+  if (s) return bail(s);
+  if (recv_peer >= 0 && recv_peer == send_peer) {
+    L->recv_base = L->send_base;   // one mapping serves both directions
+  } else if ((s = open_peer(recv_peer, &L->recv_base, &L->recv_ipc))) {
+    return bail(s);
+  }
+  *out = L;
+  return OCC_OK;
+}
+
+extern "C" occ_status occ_link_close(occ_link L) {
+  if (!L) return OCC_OK;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (L->send_ipc) cudaIpcCloseMemHandle(L->send_base);
+  if (L->recv_ipc && L->recv_base != L->send_base) cudaIpcCloseMemHandle(L->recv_base);
+  cudaFree(L->local);
+  delete L;
+  return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_link_close");
+}
+
+extern "C" occ_status occ_sendrecv_factors_link(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, occ_mat out,
+                                                occ_mat Prcv, occ_mat Qrcv, uint32_t flags, occ_link L, void* ws,
+                                                size_t ws_bytes, cudaStream_t stream) {
+  NvtxRange nvtx_("occ_sendrecv_factors_link");
+  if (!L) return fail(OCC_ERR_INVALID_ARG, "link is null");
+  if (r != L->r) return fail(OCC_ERR_RANK, "rank %d differs from the link's %d", r, L->r);
+  const bool snd = L->send_peer >= 0, rcv = L->recv_peer >= 0;
+  const bool compress = snd && M.ptr != nullptr, decompress = rcv && out.ptr != nullptr;
+  const bool ot = (flags & OCC_ORIENT_T) != 0;
+  occ_status s;
+  // every argument check before anything is enqueued
+  if (compress) {
+    if ((s = check_step(M, err, Q, P, nullptr, r, flags))) return s;
+  } else if (snd) {
+    if ((s = check_rank(r, P.rows, Q.rows))) return s;
+    if ((s = check_view(P, "P", P.rows, r, true, true))) return s;
+    if ((s = check_view(Q, "Q", Q.rows, r, true, true))) return s;
+  }
+  if (snd && P.rows + Q.rows > L->cap_rows)
+    return fail(OCC_ERR_SHAPE, "factors of %lld + %lld rows exceed the link's %lld", (long long)P.rows,
+                (long long)Q.rows, (long long)L->cap_rows);
+  if (decompress) {
+    const occ_mat sb[4] = {M, err, Q, P};
+    if ((s = check_recv_side(out, Prcv, Qrcv, r, flags & ~(uint32_t)OCC_WIRE_BF16, sb, snd ? 4 : 0))) return s;
+  } else if (rcv) {
+    if ((s = check_view(Prcv, "Prcv", Prcv.rows, r, true, true))) return s;
+    if ((s = check_view(Qrcv, "Qrcv", Qrcv.rows, r, true, true))) return s;
+    if (overlap(Prcv, Qrcv)) return fail(OCC_ERR_ALIAS, "Prcv and Qrcv overlap");
+  }
+  if (rcv && Prcv.rows + Qrcv.rows > L->cap_rows) return fail(OCC_ERR_SHAPE, "received factors exceed the link");
+  cudaError_t e = cudaSuccess;
+  if (snd) {
+    const unsigned seq = ++L->send_seq;
+    LinkPush push;
+    push.P = reinterpret_cast<float*>(L->send_base + (seq & 1u) * L->slot_bytes);
+    push.Q = push.P + (size_t)P.rows * r;
+    push.flag = link_word(L->send_base, L, kLinkFlag);
+    push.ack = link_word(L->local, L, kLinkAck);
+    push.ctr = link_word(L->local, L, kLinkPushCtr);
+    push.seq = seq;
+    bool pushed = false;
+    if (compress) {
+      occ_mat none = {nullptr, 0, 0, 0, M.dtype};
+      if ((s = compress_impl(M, err, Q, P, none, r, flags, ws, ws_bytes, stream, &push, &pushed))) return s;
+    }
+    if (!pushed)
+      e = run_link_copy(static_cast<const float*>(P.ptr), static_cast<const float*>(Q.ptr), push.P, push.Q,
+                        (long long)P.rows * r, (long long)Q.rows * r, seq > 2 ? push.ack : nullptr, seq - 2,
+                        push.ctr, push.flag, seq, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "link push");
+  }
+  if (rcv) {
+    const unsigned seq = ++L->recv_seq;
+    float* Pm = reinterpret_cast<float*>(L->local + (seq & 1u) * L->slot_bytes);
+    float* Qm = Pm + (size_t)Prcv.rows * r;
+    LinkRecv lr;
+    lr.wait_flag = link_word(L->local, L, kLinkFlag);
+    lr.seq = seq;
+    lr.ack = link_word(L->recv_base, L, kLinkAck);
+    lr.ctr = link_word(L->local, L, kLinkRecvCtr);
+    if (decompress) {
+      // the kernel's P operand is the row-side factor: P_hat, or Q with OCC_ORIENT_T (out = Q P^T)
+      const float* kP = ot ? Qm : Pm;
+      const float* kQ = ot ? Pm : Qm;
+      lr.copyP = static_cast<float*>(ot ? Qrcv.ptr : Prcv.ptr);
+      lr.copyQ = static_cast<float*>(ot ? Prcv.ptr : Qrcv.ptr);
+      lr.nP = (long long)(ot ? Qrcv.rows : Prcv.rows) * r;
+      lr.nQ = (long long)(ot ? Prcv.rows : Qrcv.rows) * r;
+      e = run_v2_decompress_link(kP, kQ, out.ptr, out.ld, (int)out.rows, (int)out.cols, r, out.dtype == OCC_BF16, lr,
+                                 stream);
+    } else {
+      e = run_link_copy(Pm, Qm, static_cast<float*>(Prcv.ptr), static_cast<float*>(Qrcv.ptr),
+                        (long long)Prcv.rows * r, (long long)Qrcv.rows * r, lr.wait_flag, seq, lr.ctr, lr.ack, seq,
+                        stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "link receive");
+  }
+  return OCC_OK;
 }

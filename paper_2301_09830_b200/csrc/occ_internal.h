@@ -53,5 +53,21 @@ cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long lo
 // A = M + e_old is loaded before M' is stored, so recon may alias M.
 cudaError_t run_v2_reconstruct(const Params& p, int r, cudaStream_t st);
 cudaError_t run_init_q(float* q, int64_t rows, int r, int64_t ld, uint64_t seed, cudaStream_t st);
+// occ_link receiver side of one step (occ_v2.cu)
+struct LinkRecv {
+  const unsigned* wait_flag;   // local flag word
+  unsigned seq;
+  unsigned* ack;               // the sender's ack word (peer memory)
+  unsigned* ctr;               // local CTA-exit counter
+  float* copyP;                // caller's Prcv / Qrcv (or nullptr)
+  float* copyQ;
+  long long nP, nQ;            // floats
+};
+cudaError_t run_v2_decompress_link(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r,
+                                   bool bf16, const LinkRecv& lr, cudaStream_t st);
+cudaError_t run_link_copy(const float* sP, const float* sQ, float* dP, float* dQ, long long nP, long long nQ,
+                          const unsigned* wait_word, unsigned wait_target, unsigned* ctr, unsigned* done_word,
+                          unsigned done_seq, cudaStream_t st);
+unsigned take_link_timeout();
 
 }  // namespace occ

@@ -50,6 +50,55 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// Sender side of one occ_link step (include/occ.h): the
+// factors go to slot seq % 2 of the peer's mailbox with NVLink stores, then
+// the peer's flag is released to seq.  P == nullptr: no push.
+struct LinkPush {
+  float* P;             // peer mailbox: P_hat (prows x R)
+  float* Q;             // peer mailbox: Q (qrows x R)
+  unsigned* flag;       // peer mailbox flag word
+  const unsigned* ack;  // local ack word (the peer's receiver releases seq after reading a slot)
+  unsigned* ctr;        // local CTA-exit counter of the push (zero between calls)
+  unsigned seq;
+};
+
+// OCC_ERR for a link wait that timed out (peer gone): read by occ_check_status.
+__device__ unsigned g_link_timeout = 0;
+
+// Wait (one thread) until *w - target >= 0 (sequence numbers, wrap-safe), with
+// system-scope acquire; gives up after ~2 s so a dead peer cannot hang the GPU.
+__device__ __forceinline__ bool link_wait_geq(const unsigned* w, unsigned target) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+    if ((int)(v - target) >= 0) return true;
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 2000000000ull) {
+      atomicOr(&g_link_timeout, 1u);
+      return false;
+    }
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void link_release(unsigned* w, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(w), "r"(v) : "memory");
+}
+// Called by ONE thread per CTA after the CTA's part of a link transfer (its
+// stores / reads done and fenced): the last CTA to arrive resets the counter and
+// releases `word` = seq to the other GPU.
+__device__ __forceinline__ void link_cta_done(unsigned* ctr, unsigned* word, unsigned seq) {
+  __threadfence_system();
+  const unsigned old = atomicAdd(ctr, 1u);
+  if (old == gridDim.x - 1) {
+    atomicExch(ctr, 0u);
+    __threadfence_system();
+    link_release(word, seq);
+  }
+}
+
 struct Params {
   const void* M; long long ldm; int m_bf16;
   const float* err_in; long long lde_in;   // nullptr => e_old = 0 (OCC_NO_EF)
@@ -85,6 +134,7 @@ struct Params {
   int wire_bf16;         // OCC_WIRE_BF16: round P_hat and Q to bf16 before the reconstruction
   int path;
   int f_tc;              // phase F on the tensor cores (occ_tc.cuh phase_F_tc; the DP paths)
+  LinkPush push;         // occ_link sender: the fused kernel pushes the factors itself
 };
 
 // ------------------------------------------------------------------ helpers
@@ -341,59 +391,100 @@ __device__ void reduce_gram(const double* __restrict__ part, int ngp, double* S)
     int a = 0, rem = q;
     while (rem >= R - a) { rem -= R - a; a++; }
     const int b = a + rem;
-    double g = 0.0;
-    for (int u = 0; u < ngp; u++) g += __ldcg(part + (size_t)u * NP + q);
+    double g = 0.0;   // fixed order; 8 partials in flight (the chain of L2 loads is the latency)
+    for (int u0 = 0; u0 < ngp; u0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) v[j] = (u0 + j < ngp) ? __ldcg(part + (size_t)(u0 + j) * NP + q) : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; j++) g += v[j];
+    }
     S[a * R + b] = g;
     S[b * R + a] = g;
   }
 }
 
 // Right-looking Cholesky of S in place (lower triangle).  With detect, stops
-// at the first degenerate column and returns 1.  Uses all threads.
+// at the first degenerate column and returns 1.  Uses all threads.  Square-
+// root free during the elimination (one barrier per column: every thread
+// reads the pivot d_j itself, the trailing update is S_ik -= S_ij S_kj / d_j),
+// then L = column j of the eliminated S scaled by d_j^-1/2 in one pass.
 template <int R>
 __device__ int chol_inplace(double* S, double* gdiag, double tau2, bool detect, int* flag) {
   for (int x = threadIdx.x; x < R; x += blockDim.x) gdiag[x] = S[x * R + x];
   if (threadIdx.x == 0) *flag = 0;
   __syncthreads();
   for (int j = 0; j < R; j++) {
-    if (threadIdx.x == 0) {
-      const double d = S[j * R + j], g = gdiag[j];
-      if (detect && (g == 0.0 || !(d >= tau2 * g))) *flag = 1;
-      else S[j * R + j] = sqrt(d > 0.0 ? d : 1e-300);
+    const double d = S[j * R + j], g = gdiag[j];
+    if (detect && (g == 0.0 || !(d >= tau2 * g))) {   // uniform: every thread reads the same d, g
+      if (threadIdx.x == 0) *flag = 1;
+      __syncthreads();
+      return 1;
     }
-    __syncthreads();
-    if (*flag) return 1;
-    const double ljj = S[j * R + j];
-    for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) S[i * R + j] /= ljj;
-    __syncthreads();
+    const double rinv = 1.0 / (d > 0.0 ? d : 1e-300);
     const int rem = R - 1 - j;
     for (int x = threadIdx.x; x < rem * rem; x += blockDim.x) {
       const int i = j + 1 + x / rem, k = j + 1 + x % rem;
-      if (k <= i) S[i * R + k] -= S[i * R + j] * S[k * R + j];
+      if (k <= i) S[i * R + k] = fma(-S[i * R + j] * rinv, S[k * R + j], S[i * R + k]);
     }
     __syncthreads();
   }
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
+    const int i = x / R, j = x % R;
+    if (j > i) continue;
+    const double d = S[j * R + j];
+    const double sd = sqrt(d > 0.0 ? d : 1e-300);
+    if (i > j) S[x] = S[x] / sd;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < R; j += blockDim.x) {
+    const double d = S[j * R + j];
+    S[j * R + j] = sqrt(d > 0.0 ? d : 1e-300);
+  }
+  __syncthreads();
   return 0;
 }
 
-// L^-1 (lower) by forward substitution, one column per thread; returns
-// kappa_est = ||L||_F * ||L^-1||_F (>= cond_2(L) = cond_2(P)).
+// L^-1 (lower) by forward substitution, one column per thread (four partial
+// sums per dot product: the chain is the latency); returns kappa_est =
+// ||L||_F * ||L^-1||_F (>= cond_2(L) = cond_2(P)), the norms reduced over the
+// column threads.
 template <int R>
 __device__ void tri_inverse(const double* S, double* Li, double* kappa_out) {
+  __shared__ double nrm[2][NT / 32];
+  double nl = 0.0, ni = 0.0;
   for (int c = threadIdx.x; c < R; c += blockDim.x) {
-    for (int i = 0; i < R; i++) Li[i * R + c] = 0.0;
+    for (int i = 0; i < c; i++) Li[i * R + c] = 0.0;
     for (int i = c; i < R; i++) {
-      double v = (i == c) ? 1.0 : 0.0;
-      for (int k = c; k < i; k++) v -= S[i * R + k] * Li[k * R + c];
-      Li[i * R + c] = v / S[i * R + i];
+      double v0 = (i == c) ? 1.0 : 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+      int k = c;
+      for (; k + 4 <= i; k += 4) {
+        v0 = fma(-S[i * R + k], Li[k * R + c], v0);
+        v1 = fma(-S[i * R + k + 1], Li[(k + 1) * R + c], v1);
+        v2 = fma(-S[i * R + k + 2], Li[(k + 2) * R + c], v2);
+        v3 = fma(-S[i * R + k + 3], Li[(k + 3) * R + c], v3);
+      }
+      for (; k < i; k++) v0 = fma(-S[i * R + k], Li[k * R + c], v0);
+      const double x = ((v0 + v1) + (v2 + v3)) / S[i * R + i];
+      Li[i * R + c] = x;
+      ni = fma(x, x, ni);
+      nl = fma(S[i * R + c], S[i * R + c], nl);   // column c of L
     }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    nl += __shfl_xor_sync(0xffffffffu, nl, off);
+    ni += __shfl_xor_sync(0xffffffffu, ni, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    nrm[0][threadIdx.x >> 5] = nl;
+    nrm[1][threadIdx.x >> 5] = ni;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double nl = 0.0, ni = 0.0;
-    for (int i = 0; i < R; i++)
-      for (int k = 0; k <= i; k++) { nl += S[i * R + k] * S[i * R + k]; ni += Li[i * R + k] * Li[i * R + k]; }
-    *kappa_out = sqrt(nl) * sqrt(ni);
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) { a += nrm[0][w]; b += nrm[1][w]; }
+    *kappa_out = sqrt(a) * sqrt(b);
   }
   __syncthreads();
 }
@@ -434,21 +525,38 @@ __device__ void chol_substitute(OrthSmem<R>& o, double tau2) {
 }
 
 // P_hat rows [r0, r0+nr) = Pm Li^T in fp64, rounded to fp32, written to dst.
-// Pm[i][b] = rep[b] ? f_b[i] : src[i][b].
+// Pm[i][b] = rep[b] ? f_b[i] : src[i][b].  Each thread forms R / KPT outputs
+// of one row (k = kg, kg + KPT, ...) with the row in registers; the Li row it
+// needs is read as 16-byte pairs (the same address across the warp: a broadcast).
 template <int R>
 __device__ void apply_rinv(const float* src, float* dst, int r0, int nr, const double* Li,
                            const int* rep, bool use_rep, unsigned long long seed, float* ps) {
+  constexpr int KPT = (R >= 16) ? R / 8 : 1;   // outputs per thread; R / KPT threads per row
+  constexpr int TPR = R / KPT;
   __syncthreads();
   for (int x = threadIdx.x; x < nr * R; x += blockDim.x) {
     const int i = x / R, b = x % R;
     ps[x] = (use_rep && rep[b]) ? fallback_entry(seed, b, r0 + i) : __ldcg(src + (size_t)r0 * R + x);
   }
   __syncthreads();
-  for (int x = threadIdx.x; x < nr * R; x += blockDim.x) {
-    const int i = x / R, a = x % R;
-    double v = 0.0;
-    for (int b = 0; b <= a; b++) v = fma((double)ps[i * R + b], Li[a * R + b], v);
-    dst[(size_t)r0 * R + x] = (float)v;
+  for (int x = threadIdx.x; x < nr * TPR; x += blockDim.x) {
+    const int i = x / TPR, kg = x % TPR;
+    float pr[R];
+#pragma unroll
+    for (int b = 0; b < R; b++) pr[b] = ps[i * R + b];
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+      const int a = kg + TPR * j;
+      const double* la = Li + a * R;
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int b = 0; b < R; b += 2) {   // Li is lower: the b > a terms are zero
+        const double2 l = *reinterpret_cast<const double2*>(la + b);
+        v0 = fma((double)pr[b], l.x, v0);
+        v1 = fma((double)pr[b + 1], l.y, v1);
+      }
+      dst[(size_t)(r0 + i) * R + a] = (float)(v0 + v1);
+    }
   }
   __syncthreads();
 }

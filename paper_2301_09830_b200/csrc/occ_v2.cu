@@ -248,6 +248,16 @@ struct DecArgs {
   long long lde_in;
   float* err_out;            // EF: e_new (lde_out); may equal err_in
   long long lde_out;
+  // occ_link receiver (non-EF): wait for the peer's flag >= wait_seq before reading
+  // P / Q (the mailbox slot), copy them to copyP / copyQ (nP, nQ floats), and
+  // release ack = wait_seq on the sender once every CTA is done with the slot
+  const unsigned* wait_flag;
+  unsigned wait_seq;
+  unsigned* ack;
+  unsigned* ctr;
+  float* copyP;
+  float* copyQ;
+  long long nP, nQ;
 };
 
 // row blocks per work item: 8, or 4 at r = 64 (the prefetched P fragment is RBI x r/8 x 2 registers);
@@ -312,6 +322,10 @@ __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs
         }
     }
   };
+  if (!EF && d.wait_flag) {   // occ_link receiver: the factors are in the mailbox once the flag says so
+    if (threadIdx.x == 0) link_wait_geq(d.wait_flag, d.wait_seq);
+    __syncthreads();
+  }
   const int stride = gridDim.x * 8;
   int item = blockIdx.x * 8 + warp;
   float qv[KS5][4], pf[RBI][KS5][2];
@@ -390,6 +404,39 @@ __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs
       }
     }
   }
+  if (!EF && d.wait_flag) {   // copy the received factors out, then acknowledge the slot
+    const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
+    if (d.copyP)
+      for (long long x = gt; x < d.nP / 4; x += gs)
+        reinterpret_cast<float4*>(d.copyP)[x] = __ldg(reinterpret_cast<const float4*>(P) + x);
+    if (d.copyQ)
+      for (long long x = gt; x < d.nQ / 4; x += gs)
+        reinterpret_cast<float4*>(d.copyQ)[x] = __ldg(reinterpret_cast<const float4*>(Q) + x);
+    __syncthreads();
+    if (threadIdx.x == 0) link_cta_done(d.ctr, d.ack, d.wait_seq);
+  }
+}
+
+// occ_link transfers without a decompression: push (sender, M == NULL: the
+// factors already in local P / Q go to the peer's slot after the slot's
+// previous use is acknowledged, then the peer's flag is released) or receive
+// only (wait for the local flag, copy the slot out to the caller's P / Q, then
+// acknowledge).  sP/sQ -> dP/dQ, nP/nQ floats (multiples of 4, 16-byte aligned).
+__global__ void __launch_bounds__(256) occ_link_copy_kernel(const float* sP, const float* sQ, float* dP, float* dQ,
+                                                            long long nP, long long nQ, const unsigned* wait_word,
+                                                            unsigned wait_target, unsigned* ctr, unsigned* done_word,
+                                                            unsigned done_seq) {
+  if (wait_word) {
+    if (threadIdx.x == 0) link_wait_geq(wait_word, wait_target);
+    __syncthreads();
+  }
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
+  for (long long x = gt; x < nP / 4; x += gs)
+    reinterpret_cast<float4*>(dP)[x] = __ldcg(reinterpret_cast<const float4*>(sP) + x);
+  for (long long x = gt; x < nQ / 4; x += gs)
+    reinterpret_cast<float4*>(dQ)[x] = __ldcg(reinterpret_cast<const float4*>(sQ) + x);
+  __syncthreads();
+  if (threadIdx.x == 0) link_cta_done(ctr, done_word, done_seq);
 }
 
 // ------------------------------------------------------------------ host side
@@ -543,6 +590,7 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
   p.amp_thr = (p.debug & 4) ? -1.0 : 32.0;
   p.check_finite = p1.check_finite;
   p.wire_bf16 = p1.wire_bf16;
+  p.push = p1.push;
   auto kern = occ_v2_kernel<R, MBF>;
   // the dynamic-SMEM opt-in only ever grows; set it when a plan needs more
   // (per device: the attribute is per-context state)
@@ -624,6 +672,32 @@ cudaError_t run_v2_decompress(const float* P, const float* Q, void* out, long lo
   v2::DecArgs d{};
   d.P = P; d.Q = Q; d.out = out; d.ldo = ldo; d.n = n; d.m = m;
   return launch_v2_decompress(d, r, bf16, false, st);
+}
+
+cudaError_t run_v2_decompress_link(const float* P, const float* Q, void* out, long long ldo, int n, int m, int r,
+                                   bool bf16, const LinkRecv& lr, cudaStream_t st) {
+  v2::DecArgs d{};
+  d.P = P; d.Q = Q; d.out = out; d.ldo = ldo; d.n = n; d.m = m;
+  d.wait_flag = lr.wait_flag; d.wait_seq = lr.seq; d.ack = lr.ack; d.ctr = lr.ctr;
+  d.copyP = lr.copyP; d.copyQ = lr.copyQ; d.nP = lr.nP; d.nQ = lr.nQ;
+  return launch_v2_decompress(d, r, bf16, false, st);
+}
+
+cudaError_t run_link_copy(const float* sP, const float* sQ, float* dP, float* dQ, long long nP, long long nQ,
+                          const unsigned* wait_word, unsigned wait_target, unsigned* ctr, unsigned* done_word,
+                          unsigned done_seq, cudaStream_t st) {
+  const long long vec = (nP + nQ) / 4;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(148, (vec + 255) / 256));
+  v2::occ_link_copy_kernel<<<grid, 256, 0, st>>>(sP, sQ, dP, dQ, nP, nQ, wait_word, wait_target, ctr, done_word,
+                                                 done_seq);
+  return cudaGetLastError();
+}
+
+unsigned take_link_timeout() {
+  unsigned v = 0, z = 0;
+  if (cudaMemcpyFromSymbol(&v, g_link_timeout, sizeof v) != cudaSuccess) return 0;
+  if (v) cudaMemcpyToSymbol(g_link_timeout, &z, sizeof z);
+  return v;
 }
 
 cudaError_t run_v2_reconstruct(const Params& p, int r, cudaStream_t st) {

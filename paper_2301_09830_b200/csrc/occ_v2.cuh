@@ -81,6 +81,7 @@ struct Params2 {
   int wire_bf16;       // OCC_WIRE_BF16: P_hat rows and the Q slice rounded to bf16 before phase 5
   int force_two_pass;
   int debug;           // bit 0: skip phase-1 compute (streaming floor measurement only)
+  LinkPush push;       // occ_link sender: warp NW-1 pushes this CTA's P_hat rows / Q slice during phase 5
 };
 
 // ------------------------------------------------------------------ grid barrier

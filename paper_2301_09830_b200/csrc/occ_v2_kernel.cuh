@@ -436,6 +436,8 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       tr(13);
       if (stamp) p.stats->t_ns[4] = gtimer();
       tr(9);
+      // occ_link: this CTA's P_hat rows and Q slice are final; warp NW-1 pushes them
+      if (p.push.P) asm volatile("bar.arrive 5, %0;" ::"r"((NCW + 1) * 32) : "memory");
       nb++;
       grid_barrier_spread(p.barl, nb, SyncCompute());
       tr(10);
@@ -551,6 +553,25 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       }
       if (stamp) p.stats->t_ns[6] = gtimer();
       tr(11);
+    } else if (p.push.P) {
+      // occ_link sender (include/occ.h): while the compute warps run phase 5, the
+      // producer warp copies this CTA's final P_hat rows (column band 0) and Q
+      // slice into slot seq % 2 of the peer's mailbox over NVLink, after the
+      // peer's receiver has acknowledged the slot's previous use (seq - 2)
+      asm volatile("bar.sync 5, %0;" ::"r"((NCW + 1) * 32) : "memory");
+      if (lane == 0 && p.push.seq > 2) link_wait_geq(p.push.ack, p.push.seq - 2);
+      __syncwarp();
+      if (active) {
+        auto copy = [&](const float* src, float* dst, int count) {   // count % 4 == 0, 16-byte aligned
+          const float4* s4 = reinterpret_cast<const float4*>(src);
+          float4* d4 = reinterpret_cast<float4*>(dst);
+          for (int x = lane; x < count / 4; x += 32) d4[x] = __ldcg(s4 + x);
+        };
+        if (T.cb == 0) copy(p.Pout + (size_t)T.row0 * R, p.push.P + (size_t)T.row0 * R, T.th * R);
+        copy(p.Qout + (size_t)(T.col0 + qs_cols.x) * R, p.push.Q + (size_t)(T.col0 + qs_cols.x) * R, nqc * R);
+      }
+      __syncwarp();
+      if (lane == 0) link_cta_done(p.push.ctr, p.push.flag, p.push.seq);
     }
     __syncthreads();
   }

@@ -76,6 +76,9 @@ def lib():
         "occ_recv_factors": ([M, M, M, c_int, c_int, u32, vp, vp], c_int),
         "occ_sendrecv_factors": ([M, M, M, M, c_int, c_int, M, M, M, c_int, u32, vp, vp, ctypes.c_size_t, vp], c_int),
         "occ_embed_sync": ([M, M, M, M, c_int, ctypes.c_float, u32, vp, vp, ctypes.c_size_t, vp], c_int),
+        "occ_link_open": ([vp, c_int, c_int, i64, i64, c_int, ctypes.POINTER(vp)], c_int),
+        "occ_link_close": ([vp], c_int),
+        "occ_sendrecv_factors_link": ([M, M, M, M, c_int, M, M, M, u32, vp, vp, ctypes.c_size_t, vp], c_int),
         "occ_get_unique_id": ([ctypes.c_char_p], c_int),
         "occ_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, c_int, c_int], c_int),
         "occ_comm_split": ([vp, c_int, c_int, ctypes.POINTER(vp)], c_int),
@@ -204,6 +207,21 @@ def occ_sendrecv_factors(M, err, Q, P, r: int, send_peer: int, out, Prcv, Qrcv, 
     return ws
 
 
+def occ_sendrecv_factors_link(M, err, Q, P, r: int, out, Prcv, Qrcv, link: "Link", flags: int = 0, ws=None,
+                              stream=None):
+    """occ_sendrecv_factors over an occ_link (NVLink peer memory, no NCCL call):
+    compress M and push (P, Q) into send_peer's mailbox from the kernel, receive
+    recv_peer's factors from our mailbox and decompress them into out.
+    M None: push P, Q as they are; out None: receive into Prcv, Qrcv only."""
+    if M is not None and ws is None:
+        ws = alloc_workspace(M.shape[0], M.shape[1], r, device=M.device)
+    _check(lib().occ_sendrecv_factors_link(mat(M), mat(err), mat(Q), mat(P), r, mat(out), mat(Prcv), mat(Qrcv),
+                                           flags, link.handle, ws.data_ptr() if ws is not None else None,
+                                           ws.numel() if ws is not None else 0, _stream(stream)),
+           "occ_sendrecv_factors_link")
+    return ws
+
+
 def occ_embed_sync(G, err, Q, P, r: int, scale: float, comm: Optional["Comm"], flags: int = 0, ws=None,
                    stream=None):
     if r > 0 and ws is None:
@@ -277,4 +295,24 @@ class Comm:
     def destroy(self):
         if self.handle:
             _check(lib().occ_comm_destroy(self.handle), "occ_comm_destroy")
+            self.handle = None
+
+
+class Link:
+    """An occ_link: this stage's NVLink mailboxes towards its pipeline
+    neighbours (include/occ.h).  open() is collective over the communicator."""
+
+    def __init__(self, handle: int):
+        self.handle = ctypes.c_void_p(handle)
+
+    @classmethod
+    def open(cls, comm: "Comm", send_peer: int, recv_peer: int, max_rows: int, max_cols: int, r: int) -> "Link":
+        h = ctypes.c_void_p()
+        _check(lib().occ_link_open(comm.handle, send_peer, recv_peer, max_rows, max_cols, r, ctypes.byref(h)),
+               "occ_link_open")
+        return cls(h.value)
+
+    def close(self):
+        if self.handle:
+            _check(lib().occ_link_close(self.handle), "occ_link_close")
             self.handle = None

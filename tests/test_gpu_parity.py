@@ -552,3 +552,56 @@ def test_single_rank_exchange_only():
         assert torch.equal(Pr, P) and torch.equal(Qr, Q)
     finally:
         comm.destroy()
+
+
+@pytest.mark.parametrize("n,m,r,flags", [
+    (1024, 3072, 16, 0),              # fused kernel: its producer warp pushes during phase 5
+    (1024, 3072, 16, "WIRE_BF16"),    # bf16-exact factors through the link
+    (640, 1024, 64, 0),               # per-phase path: the push kernel
+    (1000, 264, 16, "ORIENT_T"),      # P m x r, Q n x r; out = Q P^T
+])
+def test_link_self_ring_matches_oracle(n, m, r, flags):
+    """occ_sendrecv_factors_link on a ring of one (the stage is its own
+    neighbour): the factors travel through the NVLink mailbox protocol (flag,
+    two slots, ack) with no NCCL call; over 5 steps (the slots are reused after
+    their acks) the received factors equal the sent ones bit for bit, the
+    decompressed M' equals the sender's own M' bit for bit (reading C8), and
+    each step matches the oracle's LEP stream."""
+    fl = getattr(occ, "OCC_" + flags) if flags else 0
+    ot = flags == "ORIENT_T"
+    comm = occ.Comm.single()
+    link = occ.Link.open(comm, 0, 0, max(n, m), max(n, m), r)
+    try:
+        Ms = synth.d3_lep_stream(n, m, 161, 5)
+        e_o = synth.e0(n, m, 162, like=Ms[0]).astype(np.float64)
+        Q_o = synth.q0(n if ot else m, r, 163).astype(np.float64)
+        Ed, Qd = to_dev(e_o), to_dev(Q_o)
+        Pd = torch.empty(m if ot else n, r, device="cuda")
+        Pr, Qr = torch.empty_like(Pd), torch.empty_like(Qd)
+        out = torch.empty(n, m, device="cuda")
+        ws = occ.alloc_workspace(n, m, r)
+        for t, Mt in enumerate(Ms):
+            Md = to_dev(Mt)
+            occ.occ_sendrecv_factors_link(Md, Ed, Qd, Pd, r, out, Pr, Qr, link, flags=fl, ws=ws)
+            occ.occ_check_status(comm=comm)
+            assert torch.equal(Pr, Pd) and torch.equal(Qr, Qd), t
+            own = torch.empty_like(out)
+            if ot:
+                occ.occ_decompress(Qd, Pd, own)
+            else:
+                occ.occ_decompress(Pd, Qd, own)
+            torch.cuda.synchronize()
+            assert torch.equal(out, own), t
+            o = oracle.compress_step(Mt, e_o, Q_o, orient_t=ot, wire_bf16=flags == "WIRE_BF16")
+            A = Mt.astype(np.float64) + e_o
+            tol = 1e-3 if flags == "WIRE_BF16" else TOL32
+            assert rel(out.double().cpu().numpy(), o["recon"], A) <= tol, t
+            e_o, Q_o = o["err"], o["Q"]
+        # exchange only: push P, Q as they are; receive without decompressing
+        P2, Q2 = torch.randn_like(Pd), torch.randn_like(Qd)
+        occ.occ_sendrecv_factors_link(None, None, Q2, P2, r, None, Pr, Qr, link)
+        occ.occ_check_status(comm=comm)
+        assert torch.equal(Pr, P2) and torch.equal(Qr, Q2)
+    finally:
+        link.close()
+        comm.destroy()
