@@ -187,3 +187,14 @@ def test_python_binding_fails_loudly_without_library(monkeypatch, tmp_path):
     monkeypatch.setattr(occ, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(RuntimeError):
         occ.lib()
+
+
+def test_link_argument_errors(L):
+    """occ_link (f1): null handles and bad peers are rejected on the host."""
+    h = ctypes.c_void_p()
+    assert status_name(L, L.occ_link_open(None, 0, 0, 16, 16, 4, ctypes.byref(h))) == "OCC_ERR_INVALID_ARG"
+    assert L.occ_link_close(None) == 0
+    M, E, Q, P = good()
+    s = L.occ_sendrecv_factors_link(M, E, Q, P, 16, M, P, Q, 0, None, ctypes.c_void_p(FAKE), 1 << 30, None)
+    assert status_name(L, s) == "OCC_ERR_INVALID_ARG"
+    assert {"occ_link_open", "occ_link_close", "occ_sendrecv_factors_link"} <= set(declared_functions())
