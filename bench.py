@@ -220,6 +220,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-target", action="store_true", help="skip the north-star T line (C2 only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="link", choices=["link", "nccl"],
+                    help="N > 1 pipeline ring: in-kernel NVLink exchange (occ_link, default) or NCCL send/recv")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -252,6 +254,8 @@ def main():
     flush = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
     comm = occ.Comm.from_process_group() if world > 1 else None
     snd_peer, rcv_peer = (rank - 1) % world, (rank + 1) % world   # pp ring
+    links = []   # occ_link per input set (N > 1 ring with --exchange link)
+    use_link = world > 1 and args.exchange == "link" and CONFIGS[args.config]["kind"] != "dp"
 
     def flush_l2():
         flush.fill_(1.0)   # write 2x L2: evicts (and writes back) everything before the timed step
@@ -283,6 +287,9 @@ def main():
         mmax = max(m for _, m in cfg["shapes"])
         ws = occ.alloc_workspace(nmax, mmax, r, nmat=len(mats), device=dev)
         kind = cfg["kind"]
+        link = occ.Link.open(comm, snd_peer, rcv_peer, nmax, mmax, r) if use_link else None
+        if link is not None:
+            links.append(link)
 
         def step(Min=None, Rout=None):
             b = mats[0]
@@ -293,6 +300,9 @@ def main():
                                           [x["E"] for x in mats], [x["Q"] for x in mats], [x["P"] for x in mats],
                                           r, 1.0 / world, comm=comm, ws=ws)
                 return M
+            if world > 1 and link is not None:
+                occ.occ_sendrecv_factors_link(M, b["E"], b["Q"], b["P"], r, R, b["Pr"], b["Qr"], link, ws=ws)
+                return R
             if world > 1:
                 occ.occ_sendrecv_factors(M, b["E"], b["Q"], b["P"], r, snd_peer, R, b["Pr"], b["Qr"], rcv_peer,
                                          comm, ws=ws)
@@ -303,7 +313,7 @@ def main():
                 return R
             occ.occ_compress(M, b["E"], b["Q"], b["P"], R, r=r, ws=ws)
             return R
-        step.mats, step.ws, step.cfg = mats, ws, cfg
+        step.mats, step.ws, step.cfg, step.link = mats, ws, cfg, link
         return step
 
     def bench_config(name, steps, warmup):
@@ -363,7 +373,7 @@ def main():
     achieved = ab / (ms * 1e-3) / 1e9
     launches, kernel_names = count_launches(res["sets"][0])
     kind = cfg["kind"]
-    parallelism = "1gpu" if world == 1 else (f"dp{world}" if kind == "dp" else f"pp-ring{world}")
+    parallelism = "1gpu" if world == 1 else (f"dp{world}" if kind == "dp" else f"pp-ring{world}" + ("-link" if use_link else "-nccl"))
 
     # ---------------------------------------------------------------- e2e
     e2e = None
@@ -430,10 +440,26 @@ def main():
                 dist.all_reduce(qb)
         else:
             b = res["sets"][0].mats[0]
+            lk = res["sets"][0].link
 
-            def xchg():   # the library's own exchange: occ_sendrecv_factors with M = NULL, out = NULL
+            def xchg_nccl():   # the library's NCCL exchange: occ_sendrecv_factors with M = NULL, out = NULL
                 occ.occ_sendrecv_factors(None, None, b["Q"], b["P"], r, snd_peer, None, b["Pr"], b["Qr"], rcv_peer,
                                          comm)
+
+            def xchg_link():   # the in-kernel NVLink exchange alone: occ_sendrecv_factors_link, M = NULL, out = NULL
+                occ.occ_sendrecv_factors_link(None, None, b["Q"], b["P"], r, None, b["Pr"], b["Qr"], lk)
+            xchg = xchg_link if lk is not None else xchg_nccl
+            nccl_reps = 20
+            for _ in range(3):
+                xchg_nccl()
+            barrier()
+            n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n0.record(stream)
+            for _ in range(nccl_reps):
+                xchg_nccl()
+            n1.record(stream)
+            barrier()
+            nccl_us = max_over_ranks(n0.elapsed_time(n1) / nccl_reps * 1e3)
         for _ in range(5):
             xchg()
         barrier()
@@ -470,11 +496,15 @@ def main():
             model_us = 2 * fbytes * (world - 1) / world / (bw["allreduce"] * 1e9) * 1e6
         else:              # one P2P message of V bytes per link
             model_us = fbytes / (bw["sendrecv"] * 1e9) * 1e6
-        comm_line = {"factor_comm_us": comm_us, "factor_bytes": fbytes, "nvlink_busbw_allreduce_GBs": bw["allreduce"],
+        comm_line = {"factor_comm_us": comm_us, "exchange": "dp-nccl" if kind == "dp" else args.exchange,
+                     "nccl_sendrecv_us": None if kind == "dp" else nccl_us,
+                     "factor_bytes": fbytes, "nvlink_busbw_allreduce_GBs": bw["allreduce"],
                      "nvlink_sendrecv_GBs": bw["sendrecv"], "model_us": model_us, "frac_of_nvlink_roofline": model_us / comm_us,
-                     "how": "DP: the two ncclAllReduce calls of occ_allreduce_factors on its bucket sizes; PP: "
-                            "occ_sendrecv_factors(M=NULL, out=NULL), the library's grouped send+recv of (P_hat, Q); "
-                            "model = PAPER.md:607 ring cost (DP) or V / measured P2P bandwidth (PP)"}
+                     "how": "DP: the two ncclAllReduce calls of occ_allreduce_factors on its bucket sizes; PP: the "
+                            "library's exchange of (P_hat, Q) alone -- occ_sendrecv_factors_link(M=NULL, out=NULL) "
+                            "(in-kernel NVLink stores + flag, --exchange link) or occ_sendrecv_factors(M=NULL, "
+                            "out=NULL) (grouped NCCL send/recv, also reported as nccl_sendrecv_us); model = "
+                            "PAPER.md:607 ring cost (DP) or V / measured P2P bandwidth (PP)"}
 
     # ---------------------------------------------------------------- north-star T beside C2
     target = None
@@ -510,7 +540,7 @@ def main():
 
     if rank == 0:
         kern = {"1gpu": "occ_v2_kernel (fused step)" if res["stats"]["path"] == 3 else "per-phase kernels",
-                "pp": "sender compress + receiver decompress kernels" + ("" if world == 1 else " + NCCL send/recv"),
+                "pp": "sender compress + receiver decompress kernels" + ("" if world == 1 else (" + in-kernel NVLink exchange" if use_link else " + NCCL send/recv")),
                 "dp": "DP step kernels + 2 NCCL allreduces"}[kind]
         cd = config_dict(name, world, parallelism)
         cd["l2"] = (f"inputs larger than L2: {res['nsets']} rotating input sets of {elems(cfg) * 12 / 1e6:.0f} MB "
@@ -539,6 +569,9 @@ def main():
         if target:
             line["north_star_target"] = target
         print(json.dumps(line), flush=True)
+    barrier()
+    for lk in links:
+        lk.close()
     if comm is not None:
         comm.destroy()
     if world > 1:

@@ -422,10 +422,26 @@ __device__ int chol_inplace(double* S, double* gdiag, double tau2, bool detect, 
       return 1;
     }
     const double rinv = 1.0 / (d > 0.0 ? d : 1e-300);
-    const int rem = R - 1 - j;
-    for (int x = threadIdx.x; x < rem * rem; x += blockDim.x) {
-      const int i = j + 1 + x / rem, k = j + 1 + x % rem;
-      if (k <= i) S[i * R + k] = fma(-S[i * R + j] * rinv, S[k * R + j], S[i * R + k]);
+    // trailing update on a 16 x 16 thread grid, NB x NB elements per thread
+    // (rows j+1+ty+16a, columns j+1+tx+16b; lower triangle only): no index
+    // division, the column-j values in registers
+    constexpr int NB = (R + 15) / 16;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    if (ty < 16) {
+      double ci[NB], ck[NB];
+#pragma unroll
+      for (int a = 0; a < NB; a++) {
+        const int i = j + 1 + ty + 16 * a, k = j + 1 + tx + 16 * a;
+        ci[a] = (i < R) ? S[i * R + j] * rinv : 0.0;
+        ck[a] = (k < R) ? S[k * R + j] : 0.0;
+      }
+#pragma unroll
+      for (int a = 0; a < NB; a++)
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+          const int i = j + 1 + ty + 16 * a, k = j + 1 + tx + 16 * b;
+          if (i < R && k <= i) S[i * R + k] = fma(-ci[a], ck[b], S[i * R + k]);
+        }
     }
     __syncthreads();
   }

@@ -179,6 +179,45 @@ def main():
             dist.all_reduce(good, op=dist.ReduceOp.MIN)
             report("pp_ring_sendrecv" + sfx, recon_rel=r_rel, bitwise_equal_to_sender=bit, ok=bool(good.item()))
 
+    # ------------------------------------------------------------------ PP ring over occ_link (f1)
+    # the same 1F1B ring with the in-kernel NVLink exchange: the compression
+    # kernel pushes (P_hat, Q) into rank - 1's mailbox, rank + 1's factors are
+    # decompressed straight from ours; 4 steps (both mailbox slots reused)
+    if world >= 2:
+        for wflags, sfx, wb, tolr, (n, m, r) in ((0, "", False, 1e-4, (1024, 3072, 16)),
+                                                  (occ.OCC_WIRE_BF16, "_wire_bf16", True, 1e-3, (1024, 3072, 16)),
+                                                  (0, "_r64_perphase", False, 1e-4, (1536, 2048, 64))):
+            steps = 4
+            snd, rcv = (rank - 1) % world, (rank + 1) % world
+            link = occ.Link.open(comm, snd, rcv, n, m, r)
+            streams = [synth.d3_lep_stream(n, m, 1500 + w, steps) for w in range(world)]
+            e0s = [synth.e0(n, m, 1600 + w, like=streams[w][0]) for w in range(world)]
+            Q0 = synth.q0(m, r, 21)
+            Ed, Qd = torch.from_numpy(e0s[rank]).to(dev), torch.from_numpy(Q0).to(dev)
+            Pd = torch.empty(n, r, device=dev)
+            out = torch.empty(n, m, device=dev)
+            Pr, Qr = torch.empty(n, r, device=dev), torch.empty(m, r, device=dev)
+            e_o, Q_o = e0s[rcv].astype(np.float64), Q0.astype(np.float64)   # the oracle follows rank + 1's stream
+            worst, bit = 0.0, True
+            for t in range(steps):
+                Md = torch.from_numpy(streams[rank][t]).to(dev)
+                occ.occ_sendrecv_factors_link(Md, Ed, Qd, Pd, r, out, Pr, Qr, link, flags=wflags)
+                own = torch.empty_like(out)
+                occ.occ_decompress(Pd, Qd, own)
+                torch.cuda.synchronize()
+                owns = gather_np(own)
+                got = out.double().cpu().numpy()
+                bit = bit and bool(np.array_equal(got, owns[rcv]))
+                o = oracle.compress_step(streams[rcv][t], e_o, Q_o, wire_bf16=wb)
+                worst = max(worst, rel(got, o["recon"], streams[rcv][t].astype(np.float64) + e_o))
+                e_o, Q_o = o["err"], o["Q"]
+            occ.occ_check_status(comm=comm)
+            link.close()
+            good = torch.tensor([1 if (worst <= tolr and bit) else 0], device=dev)
+            dist.all_reduce(good, op=dist.ReduceOp.MIN)
+            report("pp_ring_link" + sfx, steps=steps, recon_rel_worst=worst, bitwise_equal_to_sender=bit,
+                   ok=bool(good.item()))
+
     # ------------------------------------------------------------------ EMB dense (fused, reading C12)
     V, h = 4096, 1024
     D = max(1, world // 2)

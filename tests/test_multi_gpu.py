@@ -78,5 +78,5 @@ def test_multi_gpu_parity():
     lines = [json.loads(x) for x in res.stdout.splitlines() if x.startswith("{")]
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     names = {x["check"] for x in lines}
-    assert {"dp_local_ef", "dp_global_ef", "pp_send_recv", "emb_dense", "emb_compressed"} <= names, lines
+    assert {"dp_local_ef", "dp_global_ef", "pp_send_recv", "pp_ring_link", "emb_dense", "emb_compressed"} <= names, lines
     assert all(x["ok"] for x in lines), lines
