@@ -219,7 +219,9 @@ occ_status occ_link_open(occ_comm pp, int send_peer, int recv_peer, int64_t max_
 occ_status occ_link_close(occ_link link);
 /* occ_sendrecv_factors over a link (same arguments and semantics, M.ptr == NULL:
  * push the factors already in P / Q; out.ptr == NULL: receive into Prcv / Qrcv
- * only).  OCC_WIRE_BF16 is allowed: the factors are bf16-exact fp32 values. */
+ * only).  A side whose arguments are all NULL (M and P; out and Prcv) is
+ * skipped this call, so a stage can send compressed while it receives dense.
+ * OCC_WIRE_BF16 is allowed: the factors are bf16-exact fp32 values. */
 occ_status occ_sendrecv_factors_link(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, occ_mat out, occ_mat Prcv,
                                      occ_mat Qrcv, uint32_t flags, occ_link link, void* ws, size_t ws_bytes,
                                      cudaStream_t stream);

@@ -940,7 +940,10 @@ extern "C" occ_status occ_sendrecv_factors_link(occ_mat M, occ_mat err, occ_mat 
   NvtxRange nvtx_("occ_sendrecv_factors_link");
   if (!L) return fail(OCC_ERR_INVALID_ARG, "link is null");
   if (r != L->r) return fail(OCC_ERR_RANK, "rank %d differs from the link's %d", r, L->r);
-  const bool snd = L->send_peer >= 0, rcv = L->recv_peer >= 0;
+  // a side whose arguments are all null is skipped this call (e.g. a pipeline
+  // stage whose send is compressed but whose receive is dense this micro-batch)
+  const bool snd = L->send_peer >= 0 && (M.ptr || P.ptr);
+  const bool rcv = L->recv_peer >= 0 && (out.ptr || Prcv.ptr);
   const bool compress = snd && M.ptr != nullptr, decompress = rcv && out.ptr != nullptr;
   const bool ot = (flags & OCC_ORIENT_T) != 0;
   occ_status s;

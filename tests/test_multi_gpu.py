@@ -80,3 +80,23 @@ def test_multi_gpu_parity():
     names = {x["check"] for x in lines}
     assert {"dp_local_ef", "dp_global_ef", "pp_send_recv", "pp_ring_link", "emb_dense", "emb_compressed"} <= names, lines
     assert all(x["ok"] for x in lines), lines
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("link", [False, True])
+def test_threed_integration(link):
+    """f2: two iterations of the 2 PP x D DP communication step (tests/threed_check.py)."""
+    torch = pytest.importorskip("torch")
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 4 if n >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "threed_check.py")] + (["--link"] if link else [])
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [json.loads(x) for x in res.stdout.splitlines() if x.startswith("{")]
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    names = {x["check"] for x in lines}
+    assert {"threed_backward_link", "threed_dp_sync_stage0", "threed_rank1_dense", "threed_embedding_sync"} <= names
+    assert all(x["ok"] for x in lines), lines
