@@ -968,6 +968,18 @@ extern "C" occ_status occ_sendrecv_factors_link(occ_mat M, occ_mat err, occ_mat 
   }
   if (rcv && Prcv.rows + Qrcv.rows > L->cap_rows) return fail(OCC_ERR_SHAPE, "received factors exceed the link");
   cudaError_t e = cudaSuccess;
+  if (snd && rcv && !compress && !decompress) {   // exchange only, both directions: one launch
+    const unsigned sseq = ++L->send_seq, rseq = ++L->recv_seq;
+    float* pP = reinterpret_cast<float*>(L->send_base + (sseq & 1u) * L->slot_bytes);
+    float* mP = reinterpret_cast<float*>(L->local + (rseq & 1u) * L->slot_bytes);
+    e = run_link_exchange(static_cast<const float*>(P.ptr), static_cast<const float*>(Q.ptr), pP, pP + (size_t)P.rows * r,
+                          (long long)P.rows * r, (long long)Q.rows * r, link_word(L->local, L, kLinkAck),
+                          link_word(L->local, L, kLinkPushCtr), link_word(L->send_base, L, kLinkFlag), sseq, mP,
+                          mP + (size_t)Prcv.rows * r, static_cast<float*>(Prcv.ptr), static_cast<float*>(Qrcv.ptr),
+                          (long long)Prcv.rows * r, (long long)Qrcv.rows * r, link_word(L->local, L, kLinkFlag),
+                          link_word(L->local, L, kLinkRecvCtr), link_word(L->recv_base, L, kLinkAck), rseq, stream);
+    return e == cudaSuccess ? OCC_OK : cuda_fail(e, "link exchange");
+  }
   if (snd) {
     const unsigned seq = ++L->send_seq;
     LinkPush push;

@@ -68,6 +68,11 @@ cudaError_t run_v2_decompress_link(const float* P, const float* Q, void* out, lo
 cudaError_t run_link_copy(const float* sP, const float* sQ, float* dP, float* dQ, long long nP, long long nQ,
                           const unsigned* wait_word, unsigned wait_target, unsigned* ctr, unsigned* done_word,
                           unsigned done_seq, cudaStream_t st);
+cudaError_t run_link_exchange(const float* sP, const float* sQ, float* pP, float* pQ, long long nP, long long nQ,
+                              const unsigned* ack_in, unsigned* push_ctr, unsigned* peer_flag, unsigned sseq,
+                              const float* mP, const float* mQ, float* dP, float* dQ, long long mnP, long long mnQ,
+                              const unsigned* flag_in, unsigned* recv_ctr, unsigned* peer_ack, unsigned rseq,
+                              cudaStream_t st);
 unsigned take_link_timeout();
 
 }  // namespace occ

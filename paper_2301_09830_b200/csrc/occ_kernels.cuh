@@ -541,38 +541,40 @@ __device__ void chol_substitute(OrthSmem<R>& o, double tau2) {
 }
 
 // P_hat rows [r0, r0+nr) = Pm Li^T in fp64, rounded to fp32, written to dst.
-// Pm[i][b] = rep[b] ? f_b[i] : src[i][b].  Each thread forms R / KPT outputs
-// of one row (k = kg, kg + KPT, ...) with the row in registers; the Li row it
-// needs is read as 16-byte pairs (the same address across the warp: a broadcast).
+// Pm[i][b] = rep[b] ? f_b[i] : src[i][b].  Each thread forms KPT consecutive
+// outputs a0 .. a0 + KPT - 1 of one row: per b, one fp32 -> fp64 conversion of
+// the row element and KPT / 2 16-byte loads of Li^T[b][a0 ..] (LiT: a transposed
+// copy of Li in shared scratch, R x R doubles).
 template <int R>
 __device__ void apply_rinv(const float* src, float* dst, int r0, int nr, const double* Li,
-                           const int* rep, bool use_rep, unsigned long long seed, float* ps) {
-  constexpr int KPT = (R >= 16) ? R / 8 : 1;   // outputs per thread; R / KPT threads per row
+                           const int* rep, bool use_rep, unsigned long long seed, float* ps, double* LiT) {
+  constexpr int KPT = (R >= 16) ? 8 : R;   // outputs per thread; R / KPT threads per row
   constexpr int TPR = R / KPT;
   __syncthreads();
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) LiT[(x % R) * R + x / R] = Li[x];
   for (int x = threadIdx.x; x < nr * R; x += blockDim.x) {
     const int i = x / R, b = x % R;
     ps[x] = (use_rep && rep[b]) ? fallback_entry(seed, b, r0 + i) : __ldcg(src + (size_t)r0 * R + x);
   }
   __syncthreads();
   for (int x = threadIdx.x; x < nr * TPR; x += blockDim.x) {
-    const int i = x / TPR, kg = x % TPR;
-    float pr[R];
+    const int i = x / TPR, a0 = (x % TPR) * KPT;
+    double acc[KPT];
 #pragma unroll
-    for (int b = 0; b < R; b++) pr[b] = ps[i * R + b];
+    for (int j = 0; j < KPT; j++) acc[j] = 0.0;
+#pragma unroll 8
+    for (int b = 0; b < R; b++) {   // Li is lower: LiT[b][a] = 0 for b > a
+      const double pb = (double)ps[i * R + b];
+      const double2* lt = reinterpret_cast<const double2*>(LiT + b * R + a0);
 #pragma unroll
-    for (int j = 0; j < KPT; j++) {
-      const int a = kg + TPR * j;
-      const double* la = Li + a * R;
-      double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-      for (int b = 0; b < R; b += 2) {   // Li is lower: the b > a terms are zero
-        const double2 l = *reinterpret_cast<const double2*>(la + b);
-        v0 = fma((double)pr[b], l.x, v0);
-        v1 = fma((double)pr[b + 1], l.y, v1);
+      for (int j = 0; j < KPT / 2; j++) {
+        const double2 l = lt[j];
+        acc[2 * j] = fma(pb, l.x, acc[2 * j]);
+        acc[2 * j + 1] = fma(pb, l.y, acc[2 * j + 1]);
       }
-      dst[(size_t)(r0 + i) * R + a] = (float)(v0 + v1);
     }
+#pragma unroll
+    for (int j = 0; j < KPT; j++) dst[(size_t)(r0 + i) * R + a0 + j] = (float)acc[j];
   }
   __syncthreads();
 }
@@ -635,7 +637,7 @@ __device__ int phase_C1(const Params& p, OrthSmem<R>& o, float* ps) {
   const bool need2 = p.force_two_pass || o.kappa > p.kappa_thr;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
-    apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, false, p.fb_seed, ps);
+    apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, false, p.fb_seed, ps, o.X);
     if (need2) gram_partial<R>(p.P, r0, nr, p.G2_part + (size_t)u * npairs(R), ps);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -665,7 +667,7 @@ __device__ int phase_C2(const Params& p, OrthSmem<R>& o, float* ps) {
   const bool need2 = p.force_two_pass || o.kappa > p.kappa_thr;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
-    apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, true, p.fb_seed, ps);
+    apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, true, p.fb_seed, ps, o.X);
     if (need2) gram_partial<R>(p.P, r0, nr, p.G2_part + (size_t)u * npairs(R), ps);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -690,7 +692,7 @@ __device__ void phase_C3(const Params& p, OrthSmem<R>& o, float* ps) {
   tri_inverse<R>(o.S, o.Li, &dummy);
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
-    apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, false, p.fb_seed, ps);
+    apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, false, p.fb_seed, ps, o.X);
   }
 }
 

@@ -439,6 +439,32 @@ __global__ void __launch_bounds__(256) occ_link_copy_kernel(const float* sP, con
   if (threadIdx.x == 0) link_cta_done(ctr, done_word, done_seq);
 }
 
+// occ_link exchange without compute in both directions, ONE launch: push the
+// local factors into the peer's slot (after the slot's ack), release the
+// peer's flag, then wait for our own flag, copy our slot out and acknowledge.
+__global__ void __launch_bounds__(256) occ_link_exchange_kernel(const float* sP, const float* sQ, float* pP, float* pQ,
+                                                                long long nP, long long nQ, const unsigned* ack_in,
+                                                                unsigned* push_ctr, unsigned* peer_flag, unsigned sseq,
+                                                                const float* mP, const float* mQ, float* dP, float* dQ,
+                                                                long long mnP, long long mnQ, const unsigned* flag_in,
+                                                                unsigned* recv_ctr, unsigned* peer_ack, unsigned rseq) {
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
+  if (threadIdx.x == 0 && sseq > 2) link_wait_geq(ack_in, sseq - 2);
+  __syncthreads();
+  for (long long x = gt; x < nP / 4; x += gs) reinterpret_cast<float4*>(pP)[x] = __ldcg(reinterpret_cast<const float4*>(sP) + x);
+  for (long long x = gt; x < nQ / 4; x += gs) reinterpret_cast<float4*>(pQ)[x] = __ldcg(reinterpret_cast<const float4*>(sQ) + x);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    link_cta_done(push_ctr, peer_flag, sseq);
+    link_wait_geq(flag_in, rseq);
+  }
+  __syncthreads();
+  for (long long x = gt; x < mnP / 4; x += gs) reinterpret_cast<float4*>(dP)[x] = __ldcg(reinterpret_cast<const float4*>(mP) + x);
+  for (long long x = gt; x < mnQ / 4; x += gs) reinterpret_cast<float4*>(dQ)[x] = __ldcg(reinterpret_cast<const float4*>(mQ) + x);
+  __syncthreads();
+  if (threadIdx.x == 0) link_cta_done(recv_ctr, peer_ack, rseq);
+}
+
 // ------------------------------------------------------------------ host side
 struct Plan2 {
   bool ok = false;
@@ -686,10 +712,23 @@ cudaError_t run_v2_decompress_link(const float* P, const float* Q, void* out, lo
 cudaError_t run_link_copy(const float* sP, const float* sQ, float* dP, float* dQ, long long nP, long long nQ,
                           const unsigned* wait_word, unsigned wait_target, unsigned* ctr, unsigned* done_word,
                           unsigned done_seq, cudaStream_t st) {
-  const long long vec = (nP + nQ) / 4;
-  const int grid = (int)std::max<long long>(1, std::min<long long>(148, (vec + 255) / 256));
+  const long long vec = (nP + nQ) / 4;   // a few CTAs: each pays a system-scope fence
+  const int grid = (int)std::max<long long>(1, std::min<long long>(32, (vec + 1023) / 1024));
   v2::occ_link_copy_kernel<<<grid, 256, 0, st>>>(sP, sQ, dP, dQ, nP, nQ, wait_word, wait_target, ctr, done_word,
                                                  done_seq);
+  return cudaGetLastError();
+}
+
+cudaError_t run_link_exchange(const float* sP, const float* sQ, float* pP, float* pQ, long long nP, long long nQ,
+                              const unsigned* ack_in, unsigned* push_ctr, unsigned* peer_flag, unsigned sseq,
+                              const float* mP, const float* mQ, float* dP, float* dQ, long long mnP, long long mnQ,
+                              const unsigned* flag_in, unsigned* recv_ctr, unsigned* peer_ack, unsigned rseq,
+                              cudaStream_t st) {
+  // a few CTAs: the transfer is small and every CTA pays a system-scope fence
+  const long long vec = std::max(nP + nQ, mnP + mnQ) / 4;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(32, (vec + 1023) / 1024));
+  v2::occ_link_exchange_kernel<<<grid, 256, 0, st>>>(sP, sQ, pP, pQ, nP, nQ, ack_in, push_ctr, peer_flag, sseq, mP, mQ,
+                                                     dP, dQ, mnP, mnQ, flag_in, recv_ctr, peer_ack, rseq);
   return cudaGetLastError();
 }
 
