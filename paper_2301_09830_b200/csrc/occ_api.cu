@@ -527,6 +527,7 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
       p.dp_local_err = dpl ? 1 : 0;
       p.recon = G[i].ptr;
       p.ldr = G[i].ld;
+      p.f_tc = 1;
       cudaError_t e = run_phases(p, g, kPhF, kPhEnd, multi, dpl, stream);
       if (e != cudaSuccess) return cuda_fail(e, "dp (ORIENT_T) reconstruct launch");
     }

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(NT, (R <= 16) ? 2 : 1) occ_step_kernel(Params 
         break;
       case P_E: phase_E<R>(p); break;
       case P_F:
-        if (p.f_tc && !p.Ploc && !p.Pstate_out) {   // the DP reconstruction (occ_tc.cuh)
+        if (p.f_tc) {   // the DP reconstruction (occ_tc.cuh), plain or OCC_ORIENT_T
           if (p.m_bf16) tc::phase_F_tc<R, DPL, true>(p, smraw);
           else tc::phase_F_tc<R, DPL, false>(p, smraw);
         } else {

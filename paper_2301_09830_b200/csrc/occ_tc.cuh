@@ -310,8 +310,10 @@ constexpr int F_TC_ROWS = 128, F_TC_COLS = 64;
 template <int R>
 __host__ __device__ constexpr size_t smem_F_tc() {
   constexpr int KS = (R + 7) / 8;
-  // P_hat: [8 m-tiles][KS][32] x 2 uint4 (hi, lo); Q_sum, Q_w: [8 n-tiles][KS][32] uint4 each
-  return (size_t)8 * KS * 32 * 32 + 2 * (size_t)8 * KS * 32 * 16;
+  // two row factors [8 m-tiles][KS][32] x 2 uint4 (hi, lo) and two column
+  // factors [8 n-tiles][KS][32] uint4: (P_hat; Q_sum, Q_w) or, with
+  // OCC_ORIENT_T, (scale V_sum, V_w; U_hat)
+  return 2 * (size_t)8 * KS * 32 * 32 + 2 * (size_t)8 * KS * 32 * 16;
 }
 
 template <int R, bool DPL, bool MBF>
@@ -319,10 +321,20 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
   constexpr int KS = (R + 7) / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int wr = warp & 3, wc = warp >> 2;
-  uint4* ph = reinterpret_cast<uint4*>(smraw);   // [mt8][ks][lane]: hi(a0..a3), then lo at + 8 KS 32
+  // row factors A1 (M'), A2 (e_new) and column factors B1 (M'), B2 (e_new):
+  //   plain:         A1 = A2 = P_hat,       B1 = scale Q_sum, B2 = Q_w (DPL)
+  //   OCC_ORIENT_T:  A1 = scale V_sum, A2 = V_w (DPL), B1 = B2 = U_hat   (reading C6; the
+  //                  row-side warm start goes to Pstate_out, which only this form sets)
+  const bool rowloc = p.Pstate_out != nullptr;
+  uint4* ph = reinterpret_cast<uint4*>(smraw);   // [mt8][ks][lane]: hi(a0..a3); lo at + 8 KS 32
   uint4* pl = ph + 8 * KS * 32;
-  uint4* qs = pl + 8 * KS * 32;                  // [nt8][ks][lane]: (h(b0), h(b1), l(b0), l(b1)) of scale Q_sum
-  uint4* qw = qs + 8 * KS * 32;                  // the same of Q_w (DPL)
+  uint4* ph2 = pl + 8 * KS * 32;
+  uint4* pl2 = ph2 + 8 * KS * 32;
+  uint4* qs = pl2 + 8 * KS * 32;                 // [nt8][ks][lane]: (h(b0), h(b1), l(b0), l(b1))
+  uint4* qw = qs + 8 * KS * 32;
+  const uint4* a2h = rowloc ? ph2 : ph;
+  const uint4* a2l = rowloc ? pl2 : pl;
+  const uint4* b2 = rowloc ? qs : qw;
   const int nrb = (p.n + F_TC_ROWS - 1) / F_TC_ROWS, ncb = (p.m + F_TC_COLS - 1) / F_TC_COLS;
   const int units = nrb * ncb;
   const bool rbf = p.r_bf16 != 0;
@@ -343,15 +355,27 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
           const int i = 32 * wr + 16 * mt + g + 8 * h, j = cl + 16 * q;
           av[mt][h][q] = ldA4<MBF>(p, R0 + i, C0 + j, p.err_out && i < nr && j < nc);
         }
-    // stage P_hat rows: P[i][k] -> m-tile i/16, ks = k/8, lane (g = i%8, t = k%4), a-slot (i%16)/8 + 2 ((k%8)/4)
+    // stage the row factors: X[i][k] -> m-tile i/16, ks = k/8, lane (g = i%8, t = k%4),
+    // a-slot (i%16)/8 + 2 ((k%8)/4); A1 = P (scaled with OCC_ORIENT_T, and the row-side warm
+    // start scale P -> Pstate_out), A2 = Ploc (OCC_ORIENT_T, DPL)
     {
       unsigned* h32 = reinterpret_cast<unsigned*>(ph);
       unsigned* l32 = reinterpret_cast<unsigned*>(pl);
+      unsigned* h232 = reinterpret_cast<unsigned*>(ph2);
+      unsigned* l232 = reinterpret_cast<unsigned*>(pl2);
+      const bool a2 = rowloc && DPL && p.Ploc;
       for (int x = threadIdx.x; x < F_TC_ROWS * KS * 2; x += occ::NT) {
         const int i = x / (KS * 2), k0 = 4 * (x % (KS * 2));
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (i < nr && k0 < R) v = __ldcg(reinterpret_cast<const float4*>(p.P + (size_t)(R0 + i) * R + k0));
-        const float vv[4] = {v.x, v.y, v.z, v.w};
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f), w = v;
+        if (i < nr && k0 < R) {
+          v = __ldcg(reinterpret_cast<const float4*>(p.P + (size_t)(R0 + i) * R + k0));
+          if (rowloc) {
+            v = make_float4(p.scale * v.x, p.scale * v.y, p.scale * v.z, p.scale * v.w);
+            if (p.Pstate_out && cb == 0) *reinterpret_cast<float4*>(p.Pstate_out + (size_t)(R0 + i) * R + k0) = v;
+          }
+          if (a2) w = __ldcg(reinterpret_cast<const float4*>(p.Ploc + (size_t)(R0 + i) * R + k0));
+        }
+        const float vv[4] = {v.x, v.y, v.z, v.w}, ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int j = 0; j < 4; j++) {
           const int k = k0 + j;
@@ -361,6 +385,11 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
           split_tf32(vv[j], hh, ll);
           h32[e] = hh;
           l32[e] = ll;
+          if (a2) {
+            split_tf32(ww[j], hh, ll);
+            h232[e] = hh;
+            l232[e] = ll;
+          }
         }
       }
     }
@@ -374,9 +403,11 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f), w = v;
         if (c < nc && k0 < R) {
           v = __ldcg(reinterpret_cast<const float4*>(p.Qrec + (size_t)(C0 + c) * R + k0));
-          v = make_float4(p.scale * v.x, p.scale * v.y, p.scale * v.z, p.scale * v.w);
-          if (p.Qstate_out && rb == 0) *reinterpret_cast<float4*>(p.Qstate_out + (size_t)(C0 + c) * R + k0) = v;
-          if (DPL) w = __ldcg(reinterpret_cast<const float4*>(p.Qloc + (size_t)(C0 + c) * R + k0));
+          if (!rowloc) {
+            v = make_float4(p.scale * v.x, p.scale * v.y, p.scale * v.z, p.scale * v.w);
+            if (p.Qstate_out && rb == 0) *reinterpret_cast<float4*>(p.Qstate_out + (size_t)(C0 + c) * R + k0) = v;
+            if (DPL) w = __ldcg(reinterpret_cast<const float4*>(p.Qloc + (size_t)(C0 + c) * R + k0));
+          }
         }
         const float vv[4] = {v.x, v.y, v.z, v.w}, ww[4] = {w.x, w.y, w.z, w.w};
         const int nt = (c >> 4) * 2 + ((c & 3) >> 1), n = 2 * ((c & 15) >> 2) + (c & 1);
@@ -388,7 +419,7 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
           split_tf32(vv[j], hh, ll);
           s32[e] = hh;
           s32[e + 2] = ll;
-          if (DPL) {
+          if (DPL && !rowloc) {
             split_tf32(ww[j], hh, ll);
             w32[e] = hh;
             w32[e + 2] = ll;
@@ -406,13 +437,18 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
         for (int q = 0; q < 4; q++) ds[mt][nt][q] = dw[mt][nt][q] = 0.f;
 #pragma unroll 2
     for (int ks = 0; ks < KS; ks++) {
-      unsigned ah[2][4], al[2][4];
+      unsigned ah[2][4], al[2][4], ah2[2][4], al2[2][4];
 #pragma unroll
       for (int mt = 0; mt < 2; mt++) {
         const size_t o = ((size_t)(2 * wr + mt) * KS + ks) * 32 + lane;
         const uint4 hv = ph[o], lv = pl[o];
         ah[mt][0] = hv.x; ah[mt][1] = hv.y; ah[mt][2] = hv.z; ah[mt][3] = hv.w;
         al[mt][0] = lv.x; al[mt][1] = lv.y; al[mt][2] = lv.z; al[mt][3] = lv.w;
+        if (DPL) {
+          const uint4 hv2 = a2h[o], lv2 = a2l[o];
+          ah2[mt][0] = hv2.x; ah2[mt][1] = hv2.y; ah2[mt][2] = hv2.z; ah2[mt][3] = hv2.w;
+          al2[mt][0] = lv2.x; al2[mt][1] = lv2.y; al2[mt][2] = lv2.z; al2[mt][3] = lv2.w;
+        }
       }
 #pragma unroll
       for (int nt = 0; nt < 4; nt++) {
@@ -421,9 +457,9 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
 #pragma unroll
         for (int mt = 0; mt < 2; mt++) mma3x(ds[mt][nt], ah[mt], al[mt], b.x, b.y, b.z, b.w);
         if (DPL) {
-          const uint4 bw = qw[o];
+          const uint4 bw = b2[o];
 #pragma unroll
-          for (int mt = 0; mt < 2; mt++) mma3x(dw[mt][nt], ah[mt], al[mt], bw.x, bw.y, bw.z, bw.w);
+          for (int mt = 0; mt < 2; mt++) mma3x(dw[mt][nt], ah2[mt], al2[mt], bw.x, bw.y, bw.z, bw.w);
         }
       }
     }

@@ -605,3 +605,31 @@ def test_link_self_ring_matches_oracle(n, m, r, flags):
     finally:
         link.close()
         comm.destroy()
+
+
+@pytest.mark.parametrize("flags", ["", "EF_GLOBAL"])
+@pytest.mark.parametrize("r", [16, 64])
+def test_dp_orient_t_single_rank_matches_oracle(flags, r):
+    """occ_allreduce_factors with OCC_ORIENT_T on a 1-rank communicator (the
+    embedding's G^T form, reading C6): the tensor-core DP reconstruction with the
+    row-side factors (scale V_sum for M', V_w for the local error) against the
+    oracle's dp_step(orient_t=True); the row-side warm start goes to Q."""
+    n, m = 1536, 512
+    fl = occ.OCC_ORIENT_T | (occ.OCC_EF_GLOBAL if flags else 0)
+    M = synth.d2_gradlike(n, m, 171)
+    e = synth.e0(n, m, 172, like=M)
+    Q0 = synth.q0(n, r, 173)
+    comm = occ.Comm.single()
+    try:
+        Gd, Ed, Qd = to_dev(M), to_dev(e), to_dev(Q0)
+        Pd = torch.empty(m, r, device="cuda")
+        occ.occ_allreduce_factors([Gd], [Ed], [Qd], [Pd], r, 1.0, flags=fl, comm=comm)
+        occ.occ_check_status(comm=comm)
+        o = oracle.dp_step([M], [e], Q0, scale=1.0, orient_t=True, ef_global=bool(flags))
+        A = M.astype(np.float64) + e
+        G = Gd.double().cpu().numpy()
+        assert rel(G, o["recon"], A) <= TOL32 and elem(G, o["recon"], A) <= TOL32 / 10
+        assert rel(Ed.double().cpu().numpy(), o["err"][0], A) <= TOL32
+        assert rel(Qd.double().cpu().numpy(), o["Q"], o["Q"]) <= 1e-3
+    finally:
+        comm.destroy()
