@@ -229,8 +229,7 @@ __device__ __noinline__ unsigned cold_orth_q(const Params2& p, Tile T, OrthW& o,
 // kernel's phase-5 arithmetic: the same 3-term TF32 split of the same fp32
 // P_hat and Q values, the same fragments and the same MMA order, so the
 // receiver's M' is bit-identical to the M' the sender's e_new was taken
-// against (reading C8).  Work item = one warp x one 16-column group x 8 row
-// blocks; the Q fragment is loaded once per item.
+// against (reading C8).  (The kernel, occ_v2_decompress_band_kernel, is below.)
 // EF = true is the sender-side reconstruction of the per-phase paths
 // (occ_compress when the fused kernel does not take the shape, OCC_ORIENT_T):
 // the same M' plus e_new = (M + e_old) - M', so every sender's e_new is taken
@@ -260,27 +259,34 @@ struct DecArgs {
   long long nP, nQ;
 };
 
-// row blocks per work item: 8, or 4 at r = 64 (the prefetched P fragment is RBI x r/8 x 2 registers);
-// with EF the next item's M and e are prefetched too (4 x RBI registers each), so fewer
-__host__ __device__ constexpr int dec_rbi(int r, bool ef) { return ef ? (r <= 16 ? 4 : 2) : (r <= 32 ? 8 : 4); }
-
+// Organised by row band: a unit is 64 rows (8 row blocks)
+// x a chunk of 8 k column groups.  The band's P_hat^T fragments (pre-split,
+// the phase-5 B operand) are staged in shared memory once per unit and reused
+// by every column group of the chunk; each warp takes column groups w, w + 8,
+// ... and loads its Q fragment once per group (one group ahead), so a lane
+// issues ~0.5 factor loads per output element instead of ~2.5.  The MMA of
+// every output cell (split3, mma3, k-steps in order) is the phase-5 one:
+// bit-identical M' (reading C8).  With EF the group's M and e are loaded
+// before its M' is stored (recon may alias M).
+constexpr int DEC_RB = 8;   // row blocks per band
 template <int R, bool BF, bool EF>
-__global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs d) {
+__global__ void __launch_bounds__(256, (R >= 64 ? 1 : 2)) occ_v2_decompress_band_kernel(const DecArgs d, int chunk_cg) {
+  constexpr int KS5 = K<R>::KS5;
   const float* __restrict__ P = d.P;
   const float* __restrict__ Q = d.Q;
   const int n = d.n, m = d.m;
-  constexpr int KS5 = K<R>::KS5, RBI = dec_rbi(R, EF);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  __shared__ uint4 pfs[DEC_RB * KS5 * 32];   // [rblk][ks][lane]: (h0, h1, l0, l1)
+  if (!EF && d.wait_flag) {   // occ_link receiver: the factors are in the mailbox once the flag says so
+    if (threadIdx.x == 0) link_wait_geq(d.wait_flag, d.wait_seq);
+    __syncthreads();
+  }
   const int ncg = (m + 15) / 16, nrb = (n + 7) / 8;
-  const int nitems = ncg * ((nrb + RBI - 1) / RBI);
-  // operands of one work item (a 16-column group x RBI row blocks), fetched one
-  // item ahead so the L2 latency overlaps the previous item's MMAs and stores
-  constexpr int RBE = EF ? RBI : 1;
-  auto fetch = [&](int item, float (&qv)[KS5][4], float (&pf)[RBI][KS5][2], float2 (&am)[RBE][2], float2 (&ae)[RBE][2]) {
-    const bool ok = item < nitems;
-    const int cg = ok ? item % ncg : 0, rb0 = ok ? (item / ncg) * RBI : nrb;
+  const int nbands = (nrb + DEC_RB - 1) / DEC_RB, nchunks = (ncg + chunk_cg - 1) / chunk_cg;
+  const int units = nbands * nchunks;
+  auto load_q = [&](int cg, float (&qv)[KS5][4]) {
     const int cl = 16 * cg + 2 * g;   // A operand Q (M = columns 2g | 2g+1, K = rank), as in phase 5
-    const bool okA = ok && cl < m, okB = ok && cl + 1 < m;
+    const bool okA = cg < ncg && cl < m, okB = cg < ncg && cl + 1 < m;
     const float* qa_ = Q + (size_t)cl * R;
 #pragma unroll
     for (int ks = 0; ks < KS5; ks++) {
@@ -290,116 +296,99 @@ __global__ void __launch_bounds__(256, 2) occ_v2_decompress_kernel(const DecArgs
       qv[ks][2] = (okA && k0 + 4 < R) ? __ldg(qa_ + k0 + 4) : 0.f;
       qv[ks][3] = (okB && k0 + 4 < R) ? __ldg(qa_ + R + k0 + 4) : 0.f;
     }
-#pragma unroll
-    for (int j = 0; j < RBI; j++) {   // B operand P_hat^T, N = rows n/2 + 4(n&1)
-      const int rn = 8 * (rb0 + j) + (g >> 1) + 4 * (g & 1);
-#pragma unroll
-      for (int ks = 0; ks < KS5; ks++) {
-        const int k = 8 * ks + t;
-        pf[j][ks][0] = (rn < n && k < R) ? __ldg(P + (size_t)rn * R + k) : 0.f;
-        pf[j][ks][1] = (rn < n && k + 4 < R) ? __ldg(P + (size_t)rn * R + k + 4) : 0.f;
-      }
+  };
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int band = u % nbands, chunk = u / nbands;
+    const int rb0 = band * DEC_RB;
+    __syncthreads();   // the previous unit's readers are done with pfs
+    for (int x = threadIdx.x; x < DEC_RB * KS5 * 32; x += blockDim.x) {   // B operand P_hat^T, N = rows n/2 + 4(n&1)
+      const int ln = x & 31, ks = (x >> 5) % KS5, j = (x >> 5) / KS5;
+      const int gg = ln >> 2, tt = ln & 3;
+      const int rn = 8 * (rb0 + j) + (gg >> 1) + 4 * (gg & 1), k = 8 * ks + tt;
+      const float p0 = (rn < n && k < R) ? __ldg(P + (size_t)rn * R + k) : 0.f;
+      const float p1 = (rn < n && k + 4 < R) ? __ldg(P + (size_t)rn * R + k + 4) : 0.f;
+      unsigned h0, l0, h1, l1;
+      split3(p0, h0, l0);
+      split3(p1, h1, l1);
+      pfs[x] = make_uint4(h0, h1, l0, l1);
     }
-    if constexpr (EF) {   // the item's M and e (rows 8 rblk + t + 4h, columns c, c + 1): in flight one item ahead
+    __syncthreads();
+    const int cg_end = min(ncg, (chunk + 1) * chunk_cg);
+    float qv[KS5][4];
+    int cg = chunk * chunk_cg + warp;
+    load_q(cg, qv);
+    for (; cg < cg_end; cg += 8) {
+      unsigned qh[KS5][4], ql[KS5][4];
+#pragma unroll
+      for (int ks = 0; ks < KS5; ks++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) split3(qv[ks][q], qh[ks][q], ql[ks][q]);
+      load_q(cg + 8 < cg_end ? cg + 8 : ncg, qv);   // next group's Q, in flight during this one
       const int c = 16 * cg + 2 * g;
 #pragma unroll
-      for (int j = 0; j < RBI; j++)
+      for (int half = 0; half < 2; half++) {
+        float2 am[4][2], ae[4][2];   // EF: A = M + e of the 4 row blocks, loaded before any store
+        if constexpr (EF) {
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int row = 8 * (rb0 + j) + t + 4 * h;
-          const bool in = ok && row < n && c < m;   // m % 8 == 0: c + 1 < m too
-          am[j][h] = make_float2(0.f, 0.f);
-          ae[j][h] = make_float2(0.f, 0.f);
-          if (in) {
-            if (d.m_bf16) {
-              am[j][h].x = __uint_as_float(__ldcs(reinterpret_cast<const unsigned*>(
-                  reinterpret_cast<const __nv_bfloat16*>(d.M) + (size_t)row * d.ldm + c)));
-            } else {
-              am[j][h] = __ldcs(reinterpret_cast<const float2*>(reinterpret_cast<const float*>(d.M) + (size_t)row * d.ldm + c));
+          for (int j = 0; j < 4; j++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int row = 8 * (rb0 + 4 * half + j) + t + 4 * h;
+              am[j][h] = ae[j][h] = make_float2(0.f, 0.f);
+              if (row < n && c < m) {   // m % 8 == 0: c + 1 < m too
+                if (d.m_bf16) {
+                  am[j][h].x = __uint_as_float(__ldcs(reinterpret_cast<const unsigned*>(
+                      reinterpret_cast<const __nv_bfloat16*>(d.M) + (size_t)row * d.ldm + c)));
+                } else {
+                  am[j][h] = __ldcs(reinterpret_cast<const float2*>(reinterpret_cast<const float*>(d.M) +
+                                                                    (size_t)row * d.ldm + c));
+                }
+                if (d.err_in) ae[j][h] = *reinterpret_cast<const float2*>(d.err_in + (size_t)row * d.lde_in + c);
+              }
             }
-            if (d.err_in) ae[j][h] = *reinterpret_cast<const float2*>(d.err_in + (size_t)row * d.lde_in + c);
+        }
+        float mrs[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          mrs[j][0] = mrs[j][1] = mrs[j][2] = mrs[j][3] = 0.f;
+#pragma unroll
+          for (int ks = 0; ks < KS5; ks++) {
+            const uint4 b = pfs[((4 * half + j) * KS5 + ks) * 32 + lane];
+            mma3(mrs[j], qh[ks], ql[ks], b.x, b.y, b.z, b.w);
           }
         }
-    }
-  };
-  if (!EF && d.wait_flag) {   // occ_link receiver: the factors are in the mailbox once the flag says so
-    if (threadIdx.x == 0) link_wait_geq(d.wait_flag, d.wait_seq);
-    __syncthreads();
-  }
-  const int stride = gridDim.x * 8;
-  int item = blockIdx.x * 8 + warp;
-  float qv[KS5][4], pf[RBI][KS5][2];
-  float2 am[RBE][2], ae[RBE][2];
-  fetch(item, qv, pf, am, ae);
-  for (; item < nitems; item += stride) {
-    const int cg = item % ncg, rb0 = (item / ncg) * RBI;
-    unsigned qh[KS5][4], ql[KS5][4];
 #pragma unroll
-    for (int ks = 0; ks < KS5; ks++)
+        for (int j = 0; j < 4; j++) {
+          const int rblk = rb0 + 4 * half + j;
+          if (rblk >= nrb || c >= m) break;
+          const int r = 8 * rblk + t;
 #pragma unroll
-      for (int q = 0; q < 4; q++) split3(qv[ks][q], qh[ks][q], ql[ks][q]);
-    float mrs[RBI][4];
-#pragma unroll
-    for (int j = 0; j < RBI; j++) {
-      mrs[j][0] = mrs[j][1] = mrs[j][2] = mrs[j][3] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < KS5; ks++) {
-        unsigned h0, l0, h1, l1;
-        split3(pf[j][ks][0], h0, l0);
-        split3(pf[j][ks][1], h1, l1);
-        mma3(mrs[j], qh[ks], ql[ks], h0, h1, l0, l1);
-      }
-    }
-    float2 cm[RBE][2], ce[RBE][2];   // this item's M and e (EF)
-#pragma unroll
-    for (int j = 0; j < RBE; j++)
-#pragma unroll
-      for (int h = 0; h < 2; h++) { cm[j][h] = am[j][h]; ce[j][h] = ae[j][h]; }
-    fetch(item + stride, qv, pf, am, ae);   // next item's operands, in flight during the stores
-#pragma unroll
-    for (int j = 0; j < RBI; j++) {
-      const int rblk = rb0 + j;
-      if (rblk >= nrb) break;
-      // mr: 0 = (row t, col 2g), 1 = (t+4, 2g), 2 = (t, 2g+1), 3 = (t+4, 2g+1)
-      const int r = 8 * rblk + t, c = 16 * cg + 2 * g;
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int row = r + 4 * h;
-        if (row >= n || c >= m) continue;
-        const bool two = c + 1 < m;
-        float v0 = mrs[j][h], v1 = mrs[j][2 + h];
-        if (BF) {   // M' as the receiver decodes it (bf16), also what e_new is taken against
-          v0 = __bfloat162float(__float2bfloat16_rn(v0));
-          v1 = __bfloat162float(__float2bfloat16_rn(v1));
-        }
-        // EF: A = M + e_old was loaded with the item's operands, BEFORE any M' of
-        // the item is stored, so recon may alias M and err_out may alias err_in
-        float a0 = 0.f, a1 = 0.f;
-        if constexpr (EF) {
-          float2 mv = cm[j][h];
-          if (d.m_bf16) {
-            const unsigned raw = __float_as_uint(cm[j][h].x);
-            mv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw));
+          for (int h = 0; h < 2; h++) {
+            const int row = r + 4 * h;
+            if (row >= n) continue;
+            float v0 = mrs[j][h], v1 = mrs[j][2 + h];
+            if (BF) {   // M' as the receiver decodes it (bf16), also what e_new is taken against
+              v0 = __bfloat162float(__float2bfloat16_rn(v0));
+              v1 = __bfloat162float(__float2bfloat16_rn(v1));
+            }
+            float a0 = 0.f, a1 = 0.f;
+            if constexpr (EF) {
+              float2 mv = am[j][h];
+              if (d.m_bf16) {
+                const unsigned raw = __float_as_uint(am[j][h].x);
+                mv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw));
+              }
+              a0 = mv.x + ae[j][h].x;
+              a1 = mv.y + ae[j][h].y;
+            }
+            if (d.out) {
+              const size_t o0 = (size_t)row * d.ldo + c;
+              if (BF) *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(d.out) + o0) = __floats2bfloat162_rn(v0, v1);
+              else *reinterpret_cast<float2*>(reinterpret_cast<float*>(d.out) + o0) = make_float2(v0, v1);
+            }
+            if constexpr (EF)
+              *reinterpret_cast<float2*>(d.err_out + (size_t)row * d.lde_out + c) = make_float2(a0 - v0, a1 - v1);
           }
-          a0 = mv.x + ce[j][h].x;
-          a1 = mv.y + ce[j][h].y;
-        }
-        if (d.out) {
-          const size_t o0 = (size_t)row * d.ldo + c;
-          if (BF) {
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(d.out) + o0;
-            if (two) *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v0, v1);
-            else dst[0] = __float2bfloat16_rn(v0);
-          } else {
-            float* dst = reinterpret_cast<float*>(d.out) + o0;
-            if (two) *reinterpret_cast<float2*>(dst) = make_float2(v0, v1);
-            else dst[0] = v0;
-          }
-        }
-        if constexpr (EF) {
-          float* dst = d.err_out + (size_t)row * d.lde_out + c;
-          if (two) *reinterpret_cast<float2*>(dst) = make_float2(a0 - v0, a1 - v1);
-          else dst[0] = a0 - v0;
         }
       }
     }
@@ -673,18 +662,22 @@ unsigned take_nonfinite_v2() {
 }
 
 static cudaError_t launch_v2_decompress(const v2::DecArgs& d, int r, bool bf16, bool ef, cudaStream_t st) {
-  const int rbi = v2::dec_rbi(r, ef);
-  const int items = ((d.m + 15) / 16) * (((d.n + 7) / 8 + rbi - 1) / rbi);
-  const int grid = std::max(1, std::min((items + 7) / 8, 148 * 2));   // persistent: 2 CTAs per SM
+  // units = 64-row bands x chunks of 8 k column groups, about 4 per CTA of a 2-per-SM persistent grid
+  const int ncg = (d.m + 15) / 16, nbands = ((d.n + 7) / 8 + v2::DEC_RB - 1) / v2::DEC_RB;
+  const long long want = 4LL * 148 * 2;
+  const int k = (int)std::max<long long>(1, std::min<long long>((ncg + 7) / 8, (long long)ncg * nbands / (8 * want)));
+  const int chunk = 8 * k;
+  const int units = nbands * ((ncg + chunk - 1) / chunk);
+  const int grid = std::max(1, std::min(units, 148 * 2));
   switch (r) {
 #define V2D(RR)                                                                                     \
   case RR:                                                                                          \
     if (ef) {                                                                                       \
-      if (bf16) v2::occ_v2_decompress_kernel<RR, true, true><<<grid, 256, 0, st>>>(d);              \
-      else v2::occ_v2_decompress_kernel<RR, false, true><<<grid, 256, 0, st>>>(d);                 \
+      if (bf16) v2::occ_v2_decompress_band_kernel<RR, true, true><<<grid, 256, 0, st>>>(d, chunk);   \
+      else v2::occ_v2_decompress_band_kernel<RR, false, true><<<grid, 256, 0, st>>>(d, chunk);      \
     } else {                                                                                        \
-      if (bf16) v2::occ_v2_decompress_kernel<RR, true, false><<<grid, 256, 0, st>>>(d);             \
-      else v2::occ_v2_decompress_kernel<RR, false, false><<<grid, 256, 0, st>>>(d);                \
+      if (bf16) v2::occ_v2_decompress_band_kernel<RR, true, false><<<grid, 256, 0, st>>>(d, chunk);  \
+      else v2::occ_v2_decompress_band_kernel<RR, false, false><<<grid, 256, 0, st>>>(d, chunk);     \
     }                                                                                               \
     return cudaGetLastError();
     V2D(4) V2D(8) V2D(16) V2D(32) V2D(64)
