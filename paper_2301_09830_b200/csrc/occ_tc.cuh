@@ -25,6 +25,8 @@
 #pragma once
 #include "occ_kernels.cuh"
 
+#include <type_traits>
+
 namespace occ {
 namespace tc {
 
@@ -332,9 +334,6 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
   uint4* pl2 = ph2 + 8 * KS * 32;
   uint4* qs = pl2 + 8 * KS * 32;                 // [nt8][ks][lane]: (h(b0), h(b1), l(b0), l(b1))
   uint4* qw = qs + 8 * KS * 32;
-  const uint4* a2h = rowloc ? ph2 : ph;
-  const uint4* a2l = rowloc ? pl2 : pl;
-  const uint4* b2 = rowloc ? qs : qw;
   const int nrb = (p.n + F_TC_ROWS - 1) / F_TC_ROWS, ncb = (p.m + F_TC_COLS - 1) / F_TC_COLS;
   const int units = nrb * ncb;
   const bool rbf = p.r_bf16 != 0;
@@ -435,34 +434,44 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
       for (int nt = 0; nt < 4; nt++)
 #pragma unroll
         for (int q = 0; q < 4; q++) ds[mt][nt][q] = dw[mt][nt][q] = 0.f;
+    auto mma_loop = [&](auto ot) {   // ot: the e_new product has its own row factor (A2)
+      constexpr bool OT = decltype(ot)::value;
 #pragma unroll 2
-    for (int ks = 0; ks < KS; ks++) {
-      unsigned ah[2][4], al[2][4], ah2[2][4], al2[2][4];
+      for (int ks = 0; ks < KS; ks++) {
+        unsigned ah[2][4], al[2][4], ah2[2][4], al2[2][4];
 #pragma unroll
-      for (int mt = 0; mt < 2; mt++) {
-        const size_t o = ((size_t)(2 * wr + mt) * KS + ks) * 32 + lane;
-        const uint4 hv = ph[o], lv = pl[o];
-        ah[mt][0] = hv.x; ah[mt][1] = hv.y; ah[mt][2] = hv.z; ah[mt][3] = hv.w;
-        al[mt][0] = lv.x; al[mt][1] = lv.y; al[mt][2] = lv.z; al[mt][3] = lv.w;
-        if (DPL) {
-          const uint4 hv2 = a2h[o], lv2 = a2l[o];
-          ah2[mt][0] = hv2.x; ah2[mt][1] = hv2.y; ah2[mt][2] = hv2.z; ah2[mt][3] = hv2.w;
-          al2[mt][0] = lv2.x; al2[mt][1] = lv2.y; al2[mt][2] = lv2.z; al2[mt][3] = lv2.w;
+        for (int mt = 0; mt < 2; mt++) {
+          const size_t o = ((size_t)(2 * wr + mt) * KS + ks) * 32 + lane;
+          const uint4 hv = ph[o], lv = pl[o];
+          ah[mt][0] = hv.x; ah[mt][1] = hv.y; ah[mt][2] = hv.z; ah[mt][3] = hv.w;
+          al[mt][0] = lv.x; al[mt][1] = lv.y; al[mt][2] = lv.z; al[mt][3] = lv.w;
+          if (OT && DPL) {
+            const uint4 hv2 = ph2[o], lv2 = pl2[o];
+            ah2[mt][0] = hv2.x; ah2[mt][1] = hv2.y; ah2[mt][2] = hv2.z; ah2[mt][3] = hv2.w;
+            al2[mt][0] = lv2.x; al2[mt][1] = lv2.y; al2[mt][2] = lv2.z; al2[mt][3] = lv2.w;
+          }
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; nt++) {
+          const size_t o = ((size_t)(4 * wc + nt) * KS + ks) * 32 + lane;
+          const uint4 b = qs[o];
+#pragma unroll
+          for (int mt = 0; mt < 2; mt++) mma3x(ds[mt][nt], ah[mt], al[mt], b.x, b.y, b.z, b.w);
+          if (DPL) {
+            if (OT) {
+#pragma unroll
+              for (int mt = 0; mt < 2; mt++) mma3x(dw[mt][nt], ah2[mt], al2[mt], b.x, b.y, b.z, b.w);
+            } else {
+              const uint4 bw = qw[o];
+#pragma unroll
+              for (int mt = 0; mt < 2; mt++) mma3x(dw[mt][nt], ah[mt], al[mt], bw.x, bw.y, bw.z, bw.w);
+            }
+          }
         }
       }
-#pragma unroll
-      for (int nt = 0; nt < 4; nt++) {
-        const size_t o = ((size_t)(4 * wc + nt) * KS + ks) * 32 + lane;
-        const uint4 b = qs[o];
-#pragma unroll
-        for (int mt = 0; mt < 2; mt++) mma3x(ds[mt][nt], ah[mt], al[mt], b.x, b.y, b.z, b.w);
-        if (DPL) {
-          const uint4 bw = b2[o];
-#pragma unroll
-          for (int mt = 0; mt < 2; mt++) mma3x(dw[mt][nt], ah2[mt], al2[mt], bw.x, bw.y, bw.z, bw.w);
-        }
-      }
-    }
+    };
+    if (rowloc) mma_loop(std::true_type{});
+    else mma_loop(std::false_type{});
     // outputs: m-tile mt, rows g (+8 h); group q: columns cl + 16 q .. + 3 =
     // (n-tile 2q: c0, c1 | n-tile 2q+1: c0, c1) for row g, (c2, c3 | c2, c3) for row g + 8
 #pragma unroll
