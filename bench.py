@@ -496,7 +496,29 @@ def main():
             model_us = 2 * fbytes * (world - 1) / world / (bw["allreduce"] * 1e9) * 1e6
         else:              # one P2P message of V bytes per link
             model_us = fbytes / (bw["sendrecv"] * 1e9) * 1e6
+        # the same step without the exchange (compress, then decompress the own
+        # factors locally): ring step - this = the exchange's cost inside the step
+        local_us = None
+        if kind != "dp":
+            sets = res["sets"]
+
+            def local_step(k):
+                b = sets[k % len(sets)].mats[0]
+                occ.occ_compress(b["M"], b["E"], b["Q"], b["P"], None, r=r, ws=sets[k % len(sets)].ws)
+                occ.occ_decompress(b["P"], b["Q"], b["R"])
+            for k in range(3):
+                local_step(k)
+            barrier()
+            l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0.record(stream)
+            for k in range(args.steps):
+                local_step(k)
+            l1.record(stream)
+            barrier()
+            local_us = max_over_ranks(l0.elapsed_time(l1) / args.steps * 1e3)
         comm_line = {"factor_comm_us": comm_us, "exchange": "dp-nccl" if kind == "dp" else args.exchange,
+                     "step_without_exchange_us": local_us,
+                     "exchange_cost_in_step_us": None if local_us is None else ms * 1e3 - local_us,
                      "nccl_sendrecv_us": None if kind == "dp" else nccl_us,
                      "factor_bytes": fbytes, "nvlink_busbw_allreduce_GBs": bw["allreduce"],
                      "nvlink_sendrecv_GBs": bw["sendrecv"], "model_us": model_us, "frac_of_nvlink_roofline": model_us / comm_us,

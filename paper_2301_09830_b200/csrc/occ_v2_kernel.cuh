@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   // one stage = SR rows of M and e: the expect_tx arrival (lane 0), then one
   // bulk copy per row and matrix, issued by 2 SR lanes of the producer warp in
   // one instruction (a single issuing thread caps a CTA at ~40 GB/s of 2 KB copies)
+  const unsigned long long pol_ef = l2_evict_first();
   auto issue = [&](int s) {
     const int slot = s % p.ns;
     const int r0 = s * SR, nrow = min(SR, T.th - r0);
@@ -102,10 +103,10 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
     if (i < nrow) {
       const size_t gi = (size_t)(T.row0 + r0 + i);
       if ((lane & 1) == 0)
-        bulk_g2s(stM + ((size_t)(slot * SR + i) * sw) * 4,
-                 reinterpret_cast<const char*>(p.M) + (gi * p.ldm + T.col0) * esz, rbM, &full[slot]);
+        bulk_g2s_hint(stM + ((size_t)(slot * SR + i) * sw) * 4,
+                      reinterpret_cast<const char*>(p.M) + (gi * p.ldm + T.col0) * esz, rbM, &full[slot], pol_ef);
       else if (p.err_in)
-        bulk_g2s(stE + (size_t)(slot * SR + i) * sw, p.err_in + gi * p.lde_in + T.col0, rbE, &full[slot]);
+        bulk_g2s_hint(stE + (size_t)(slot * SR + i) * sw, p.err_in + gi * p.lde_in + T.col0, rbE, &full[slot], pol_ef);
     }
   };
   // Q_prev^T fragments (A operand, 3-term split) of this warp's k-steps
@@ -520,16 +521,17 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
                 const size_t ro = (size_t)(8 * jj) * p.ldr, eo = (size_t)(8 * jj) * p.lde_out;
                 if (HASR) {
                   if (MBF) {
-                    *reinterpret_cast<__nv_bfloat162*>(rp + ro) = __floats2bfloat162_rn(mr[0], mr[2]);
-                    *reinterpret_cast<__nv_bfloat162*>(rp + ro + r4) = __floats2bfloat162_rn(mr[1], mr[3]);
+                    const __nv_bfloat162 b0 = __floats2bfloat162_rn(mr[0], mr[2]), b1 = __floats2bfloat162_rn(mr[1], mr[3]);
+                    st_b32_hint(rp + ro, *reinterpret_cast<const unsigned*>(&b0), pol_ef);
+                    st_b32_hint(rp + ro + r4, *reinterpret_cast<const unsigned*>(&b1), pol_ef);
                   } else {
-                    *reinterpret_cast<float2*>(rp + ro) = make_float2(mr[0], mr[2]);
-                    *reinterpret_cast<float2*>(rp + ro + r4) = make_float2(mr[1], mr[3]);
+                    st_f2_hint(reinterpret_cast<float*>(rp + ro), make_float2(mr[0], mr[2]), pol_ef);
+                    st_f2_hint(reinterpret_cast<float*>(rp + ro + r4), make_float2(mr[1], mr[3]), pol_ef);
                   }
                 }
                 if (HASE) {
-                  *reinterpret_cast<float2*>(ep + eo) = sub2(make_float2(v[0], v[2]), make_float2(mr[0], mr[2]));
-                  *reinterpret_cast<float2*>(ep + eo + e4) = sub2(make_float2(v[1], v[3]), make_float2(mr[1], mr[3]));
+                  st_f2_hint(ep + eo, sub2(make_float2(v[0], v[2]), make_float2(mr[0], mr[2])), pol_ef);
+                  st_f2_hint(ep + eo + e4, sub2(make_float2(v[1], v[3]), make_float2(mr[1], mr[3])), pol_ef);
                 }
               } else {
                 store_cell_edge<MBF>(p, T, 8 * rblk + t, c, make_float4(mr[0], mr[1], mr[2], mr[3]),
