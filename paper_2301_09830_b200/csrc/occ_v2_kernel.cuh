@@ -368,9 +368,12 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (w == NW - 1) {
     asm volatile("bar.sync 3, %0;" ::"r"((NWA + 1) * 32) : "memory");
     if (p.check_finite && blockIdx.x == 0 && lane < R && !isfinite(o.gdiag[lane])) atomicOr(&g_nonfinite_v2, 1u);
-    deg = ldl_inv_warp<R>(o, p.tau * p.tau) != 0;   // LDL^T and Li in one rolled loop
+    deg = ldl_warp_unrolled<R>(o, p.tau * p.tau, true) != 0;
     trw(8);
-    trw(15);
+    if (!deg) {
+      inverse_warp_unrolled<R>(o);
+      trw(15);
+    }
   } else {
     if (in_group_a(w)) {
       reduce_partials<R>(p.G_band, p.nr, o, gscr, group_a_index(), NWA * 32, SyncGroupA());

@@ -236,94 +236,6 @@ __device__ void inverse_warp(OrthW& o) {
   __syncwarp();
 }
 
-// LDL^T and D^-1/2 L^-1 in ONE rolled loop (the hot path): lane i holds row i
-// of the active Gram (shifted, as ldl_warp) AND column i of X = L^-1 (also
-// shifted: xr[k] = X[j+k][i] at step j).  Step j's multipliers l_{j+k,j} are
-// the broadcast column o.col[j+k] / d_j, which both updates use, so the
-// inverse needs no second chain.  The loop body is small: this code runs once
-// per call from a cold instruction cache, where the unrolled LDL + inverse
-// pair (~13 KB of straight-line code) costs ~3.8 us of fetch; rolled, only the
-// first iteration misses.  Then one pass forms Li = D^-1/2 X, kappa, amp.
-// Same protocol as ldl_warp_unrolled + inverse_warp_unrolled (o.prog = R + 2
-// when Li, kappa, amp are ready; -1 when a column is degenerate) and the same
-// outputs (o.L unit lower, o.D, o.dinv, o.Li, kappa, amp); fp64 throughout.
-template <int R>
-__device__ int ldl_inv_warp(OrthW& o, double tau2) {
-  const int i = threadIdx.x & 31;
-  double rr[R], xr[R];
-#pragma unroll
-  for (int k = 0; k < R; k++) {
-    rr[k] = (i < R) ? o.L[i * LD + k] : 0.0;
-    xr[k] = (k == i) ? 1.0 : 0.0;
-  }
-  int deg = 0;
-#pragma unroll 1
-  for (int j = 0; j < R; j++) {
-    if (i >= j && i < R) o.col[i] = rr[0];   // a_ij of the current Schur complement (= column j)
-    __syncwarp();
-    const double d = o.col[j];
-    const double gj = o.gdiag[j];
-    if (gj == 0.0 || !(d >= tau2 * gj)) { deg = 1; break; }
-    const double rinv = rcp_fast(d > 0.0 ? d : 1e-300);
-    double cv[R - 1];
-    const double* cj = o.col + j;
-#pragma unroll
-    for (int k = 1; k < R; k++) cv[k - 1] = (R <= 16 || j + k < 32) ? cj[k] : 0.0;   // a_{j+k, j}
-    const double lij = (i > j && i < R) ? rr[0] * rinv : 0.0;
-    const double xj = xr[0];                 // X[j][i]: final
-    const double xs = xj * rinv;
-    if (i < R) o.Li[j * LD + i] = xj;
-#pragma unroll
-    for (int k = 1; k < R; k++) {
-      rr[k - 1] = fma(-lij, cv[k - 1], rr[k]);   // a_{i,j+k} -= l_ij a_{j+k,j}
-      xr[k - 1] = fma(-cv[k - 1], xs, xr[k]);    // X[j+k][i] -= l_{j+k,j} X[j][i]
-    }
-    rr[R - 1] = 0.0;
-    xr[R - 1] = 0.0;
-    if (i > j && i < R) o.L[i * LD + j] = lij;
-    if (i == j) o.D[j] = d;
-    __syncwarp();
-  }
-  if (deg) {
-    __syncwarp();
-    if (i == 0) prog_release(o, -1);
-    return 1;
-  }
-  if (i < R) {
-#pragma unroll 1
-    for (int k = i; k < R; k++) o.L[i * LD + k] = (k == i) ? 1.0 : 0.0;
-    o.dinv[i] = 1.0 / sqrt(o.D[i]);
-  }
-  __syncwarp();
-  // Li[r][c] = X[r][c] d_r^-1/2 (lane c: column c); kappa = ||L D^1/2||_F ||Li||_F; amp = ||S Li^T||_F
-  double nl = 0.0, ni = 0.0;
-  if (i < R) {
-    const double sdc = sqrt(o.D[i] > 0.0 ? o.D[i] : 0.0);
-#pragma unroll 1
-    for (int r = 0; r < R; r++) {
-      const double v = o.Li[r * LD + i] * o.dinv[r];
-      o.Li[r * LD + i] = v;
-      ni = fma(v, v, ni);
-      const double lc = o.L[r * LD + i] * sdc;   // (L D^1/2)[r][c]
-      nl = fma(lc, lc, nl);
-    }
-  }
-  double na = (i < R) ? o.gdiag[i] * ni : 0.0;
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    nl += __shfl_xor_sync(0xffffffffu, nl, off);
-    ni += __shfl_xor_sync(0xffffffffu, ni, off);
-    na += __shfl_xor_sync(0xffffffffu, na, off);
-  }
-  if (i == 0) {
-    o.kappa = sqrt(nl) * sqrt(ni);
-    o.amp = sqrt(na);
-  }
-  __syncwarp();
-  if (i == 0) prog_release(o, R + 2);
-  return 0;
-}
-
 // The same factorisation fully unrolled (register rows, static indices): the
 // dynamic instruction count is ~35% lower than the rotated loop's (3.9k vs
 // 6.0k cycles for R = 16, tools/la_bench.cu), at ~1.2k more instructions of
