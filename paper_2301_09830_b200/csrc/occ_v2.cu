@@ -526,13 +526,11 @@ static Plan2 plan_search(int64_t n, int64_t m, int sms, bool mbf) {
     constexpr int KREG = QREG ? (R <= 8 ? 8 : 4) : 1;
     if (QREG && (W / 8 + NCW - 1) / NCW > KREG) continue;   // Q_prev fragments must fit the registers
     const int qs_bytes = QREG ? 0 : al128(W * RP * 4);
-    // per-warp P partials of the stages in flight (a ring entry per staging slot)
-    auto red_for = [&](int k) { return al128(k * NCW * SR * RP * 4); };
+    const int red_bytes = al128(NCW * ((H + 7) / 8 * 8) * RP * 4);   // per-warp P partials of every tile row
     int ns = 0;
     for (int k = MAX_STAGES; k >= 2; k--)
-      if (2 * k * stage_bytes + qs_bytes + red_for(k) <= smem_cap) { ns = k; break; }
+      if (2 * k * stage_bytes + qs_bytes + red_bytes <= smem_cap) { ns = k; break; }
     if (!ns) continue;
-    const int red_bytes = red_for(ns);
     pl.ns = ns;
     int off = 0;
     pl.off_stm = off; off += ns * stage_bytes;

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   unsigned char* stM = sm + p.off_stm;
   float* stE = reinterpret_cast<float*>(sm + p.off_ste);  // e, then A = M + e
   float* qs = reinterpret_cast<float*>(sm + p.off_qs);    // [W][RP] Q_prev slice (r > 16)
-  float* red = reinterpret_cast<float*>(sm + p.off_red);  // [ns][NCW][8][RP] per-warp P partials of the ring's stages
+  float* red = reinterpret_cast<float*>(sm + p.off_red);  // [NCW][nrblk][8][RP] per-warp P partials
   const int nst = active ? T.nrblk : 0;
   const size_t esz = MBF ? 2 : 4;
   uint64_t* full = mbar;
@@ -128,29 +128,10 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   if (w == NW - 1) {
     // ---------------- producer
     if (active) {   // the whole producer warp (copies issued by 2 SR lanes)
-      // P_part rows of stage sr: the sum of the NCW warp partials in its ring entry (fixed order)
-      auto reduce_stage = [&](int sr) {
-        const int slot = sr % p.ns, nrow = min(SR, T.th - sr * SR);
-        const float* base = red + (size_t)slot * NCW * SR * RP;
-        for (int x = lane; x < nrow * R; x += 32) {
-          const int i = x / R, k = x % R;
-          float v0 = 0.f, v1 = 0.f;
-#pragma unroll
-          for (int ww = 0; ww < NCW; ww++) {
-            const float q = base[((size_t)ww * SR + i) * RP + k];
-            if (ww & 1) v1 += q; else v0 += q;
-          }
-          p.P_part[((size_t)T.cb * p.n + T.row0 + sr * SR + i) * R + k] = v0 + v1;
-        }
-        __syncwarp();
-      };
-      for (int s = 0; s < nst + p.ns; s++) {
+      for (int s = 0; s < nst; s++) {
         const int slot = s % p.ns;
-        if (s >= p.ns) {   // every consumer warp is done with stage s - ns: reduce it, then reuse the slot
-          mbar_wait(&empty[slot], (unsigned)(((s / p.ns) - 1) & 1));
-          reduce_stage(s - p.ns);
-        }
-        if (s < nst) issue(s);
+        if (s >= p.ns) mbar_wait(&empty[slot], (unsigned)(((s / p.ns) - 1) & 1));
+        issue(s);
       }
     }
   } else {
@@ -276,10 +257,11 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
           const float2 x0 = A2(t, c), x1 = A2(t + 4, c);
           tmem_st4(taddr_w + (unsigned)(cs * 4), x0.x, x1.x, x0.y, x1.y);
         }
-        // this warp's partial P^T for rows 8s..8s+7 -> the slot's partial ring entry; the
-        // producer reduces the NCW partials of the stage before it refills the slot
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);   // this warp is done with the slot
+        // this warp's partial P^T for rows 8s..8s+7 -> its own slot (reduced once after the loop)
         // D[k][row]: c0 = (k=16mt+g, row=2t), c1 = (g, 2t+1), c2 = (g+8, 2t), c3 = (g+8, 2t+1)
-        float* rw = red + ((size_t)slot * NCW + w) * SR * RP;
+        float* rw = red + ((size_t)w * nst + s) * SR * RP;
 #pragma unroll
         for (int mt = 0; mt < MT; mt++) {
           float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
@@ -293,13 +275,24 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
             rw[(2 * t + 1) * RP + k0 + 8] = a3;
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);   // slot and partials released (arrive: release semantics)
         if (++slot == p.ns) { slot = 0; par ^= 1u; }
       }
     };
     if (p.err_in) consume(std::true_type{});
     else consume(std::false_type{});
+    consumer_sync();
+    // P_part rows of this tile: sum of the NCW warp partials (fixed order)
+    for (int x = tid; x < T.th * R; x += NCW * 32) {
+      const int i = x / R, k = x % R;
+      const float* rr = red + (size_t)i * RP + k;   // row i = stage i/8, row-in-stage i%8
+      float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < NCW; ww++) {
+        const float q = rr[(size_t)ww * nst * SR * RP];
+        if (ww & 1) v1 += q; else v0 += q;
+      }
+      p.P_part[((size_t)T.cb * p.n + T.row0 + i) * R + k] = v0 + v1;
+    }
   }
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   if (stamp) p.stats->t_ns[8] = wait_ns;
