@@ -308,14 +308,13 @@ __device__ void phase_D_tc(const Params& p, unsigned char* smraw) {
 // they are staged.  (Not the receiver-side arithmetic of reading C8: a DP
 // group has no receiver; every rank runs this same code on the same P_hat and
 // Q_sum, so M' is identical on all ranks.)
-constexpr int F_TC_ROWS = 128, F_TC_COLS = 64;
+constexpr int F_TC_ROWS = 128, F_TC_COLS = 128;
 template <int R>
 __host__ __device__ constexpr size_t smem_F_tc() {
   constexpr int KS = (R + 7) / 8;
-  // two row factors [8 m-tiles][KS][32] x 2 uint4 (hi, lo) and two column
-  // factors [8 n-tiles][KS][32] uint4: (P_hat; Q_sum, Q_w) or, with
-  // OCC_ORIENT_T, (scale V_sum, V_w; U_hat)
-  return 2 * (size_t)8 * KS * 32 * 32 + 2 * (size_t)8 * KS * 32 * 16;
+  // A1 [8 m-tiles][KS][32] x 2 uint4 (hi, lo); X = A2 (same size, OCC_ORIENT_T) or B2
+  // [16 n-tiles][KS][32] uint4 (plain DP); B1 [16 n-tiles][KS][32] uint4
+  return (size_t)48 * KS * 32 * 16;
 }
 
 template <int R, bool DPL, bool MBF>
@@ -330,10 +329,10 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
   const bool rowloc = p.Pstate_out != nullptr;
   uint4* ph = reinterpret_cast<uint4*>(smraw);   // [mt8][ks][lane]: hi(a0..a3); lo at + 8 KS 32
   uint4* pl = ph + 8 * KS * 32;
-  uint4* ph2 = pl + 8 * KS * 32;
+  uint4* ph2 = pl + 8 * KS * 32;                 // X region: A2 (OCC_ORIENT_T) ...
   uint4* pl2 = ph2 + 8 * KS * 32;
-  uint4* qs = pl2 + 8 * KS * 32;                 // [nt8][ks][lane]: (h(b0), h(b1), l(b0), l(b1))
-  uint4* qw = qs + 8 * KS * 32;
+  uint4* qw = ph2;                               // ... or B2 (plain DP): [nt16][ks][lane]
+  uint4* qs = pl2 + 8 * KS * 32;                 // B1 [nt16][ks][lane]: (h(b0), h(b1), l(b0), l(b1))
   const int nrb = (p.n + F_TC_ROWS - 1) / F_TC_ROWS, ncb = (p.m + F_TC_COLS - 1) / F_TC_COLS;
   const int units = nrb * ncb;
   const bool rbf = p.r_bf16 != 0;
@@ -342,18 +341,21 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
     const int R0 = rb * F_TC_ROWS, C0 = cb * F_TC_COLS;
     const int nr = min(F_TC_ROWS, p.n - R0), nc = min(F_TC_COLS, p.m - C0);
     __syncthreads();
-    // this lane's A = M + e (2 m-tiles x rows g, g+8 x 2 column groups): in flight during the staging
+    // this lane's A = M + e for one 64-column half (2 m-tiles x rows g, g + 8 x 2 column groups)
     A4 av[2][2][2];
-    const int cl = 32 * wc + 4 * t;   // first column of group 0 within the unit
+    const int cl = 32 * wc + 4 * t;   // first column of group 0 within a half
+    auto load_av = [&](int hf) {
 #pragma unroll
-    for (int mt = 0; mt < 2; mt++)
+      for (int mt = 0; mt < 2; mt++)
 #pragma unroll
-      for (int h = 0; h < 2; h++)
+        for (int h = 0; h < 2; h++)
 #pragma unroll
-        for (int q = 0; q < 2; q++) {
-          const int i = 32 * wr + 16 * mt + g + 8 * h, j = cl + 16 * q;
-          av[mt][h][q] = ldA4<MBF>(p, R0 + i, C0 + j, p.err_out && i < nr && j < nc);
-        }
+          for (int q = 0; q < 2; q++) {
+            const int i = 32 * wr + 16 * mt + g + 8 * h, j = 64 * hf + cl + 16 * q;
+            av[mt][h][q] = ldA4<MBF>(p, R0 + i, C0 + j, p.err_out && i < nr && j < nc);
+          }
+    };
+    load_av(0);   // in flight during the staging
     // stage the row factors: X[i][k] -> m-tile i/16, ks = k/8, lane (g = i%8, t = k%4),
     // a-slot (i%16)/8 + 2 ((k%8)/4); A1 = P (scaled with OCC_ORIENT_T, and the row-side warm
     // start scale P -> Pstate_out), A2 = Ploc (OCC_ORIENT_T, DPL)
@@ -392,7 +394,7 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
         }
       }
     }
-    // stage Q columns: Q[c][k] -> n-tile (c / 16) * 2 + (c % 4) / 2, n = 2 ((c % 16) / 4) + c % 2,
+    // stage the column factors: Q[c][k] -> n-tile (c / 16) * 2 + (c % 4) / 2, n = 2 ((c % 16) / 4) + c % 2,
     // ks = k / 8, lane (g = n, t = k % 4), b-slot (k % 8) / 4
     {
       unsigned* s32 = reinterpret_cast<unsigned*>(qs);
@@ -427,95 +429,100 @@ __device__ void phase_F_tc(const Params& p, unsigned char* smraw) {
       }
     }
     __syncthreads();
-    float ds[2][4][4], dw[2][4][4];
 #pragma unroll
-    for (int mt = 0; mt < 2; mt++)
+    for (int hf = 0; hf < 2; hf++) {
+      if (hf == 1) load_av(1);   // (after half 0's stores; in flight during half 1's MMAs)
+      float ds[2][4][4], dw[2][4][4];
 #pragma unroll
-      for (int nt = 0; nt < 4; nt++)
+      for (int mt = 0; mt < 2; mt++)
 #pragma unroll
-        for (int q = 0; q < 4; q++) ds[mt][nt][q] = dw[mt][nt][q] = 0.f;
-    auto mma_loop = [&](auto ot) {   // ot: the e_new product has its own row factor (A2)
-      constexpr bool OT = decltype(ot)::value;
+        for (int nt = 0; nt < 4; nt++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) ds[mt][nt][q] = dw[mt][nt][q] = 0.f;
+      const int ntb = 8 * hf + 4 * wc;   // this warp's first n-tile
+      auto mma_loop = [&](auto ot) {   // ot: the e_new product has its own row factor (A2)
+        constexpr bool OT = decltype(ot)::value;
 #pragma unroll 2
-      for (int ks = 0; ks < KS; ks++) {
-        unsigned ah[2][4], al[2][4], ah2[2][4], al2[2][4];
+        for (int ks = 0; ks < KS; ks++) {
+          unsigned ah[2][4], al[2][4], ah2[2][4], al2[2][4];
 #pragma unroll
-        for (int mt = 0; mt < 2; mt++) {
-          const size_t o = ((size_t)(2 * wr + mt) * KS + ks) * 32 + lane;
-          const uint4 hv = ph[o], lv = pl[o];
-          ah[mt][0] = hv.x; ah[mt][1] = hv.y; ah[mt][2] = hv.z; ah[mt][3] = hv.w;
-          al[mt][0] = lv.x; al[mt][1] = lv.y; al[mt][2] = lv.z; al[mt][3] = lv.w;
-          if (OT && DPL) {
-            const uint4 hv2 = ph2[o], lv2 = pl2[o];
-            ah2[mt][0] = hv2.x; ah2[mt][1] = hv2.y; ah2[mt][2] = hv2.z; ah2[mt][3] = hv2.w;
-            al2[mt][0] = lv2.x; al2[mt][1] = lv2.y; al2[mt][2] = lv2.z; al2[mt][3] = lv2.w;
-          }
-        }
-#pragma unroll
-        for (int nt = 0; nt < 4; nt++) {
-          const size_t o = ((size_t)(4 * wc + nt) * KS + ks) * 32 + lane;
-          const uint4 b = qs[o];
-#pragma unroll
-          for (int mt = 0; mt < 2; mt++) mma3x(ds[mt][nt], ah[mt], al[mt], b.x, b.y, b.z, b.w);
-          if (DPL) {
-            if (OT) {
-#pragma unroll
-              for (int mt = 0; mt < 2; mt++) mma3x(dw[mt][nt], ah2[mt], al2[mt], b.x, b.y, b.z, b.w);
-            } else {
-              const uint4 bw = qw[o];
-#pragma unroll
-              for (int mt = 0; mt < 2; mt++) mma3x(dw[mt][nt], ah[mt], al[mt], bw.x, bw.y, bw.z, bw.w);
+          for (int mt = 0; mt < 2; mt++) {
+            const size_t o = ((size_t)(2 * wr + mt) * KS + ks) * 32 + lane;
+            const uint4 hv = ph[o], lv = pl[o];
+            ah[mt][0] = hv.x; ah[mt][1] = hv.y; ah[mt][2] = hv.z; ah[mt][3] = hv.w;
+            al[mt][0] = lv.x; al[mt][1] = lv.y; al[mt][2] = lv.z; al[mt][3] = lv.w;
+            if (OT && DPL) {
+              const uint4 hv2 = ph2[o], lv2 = pl2[o];
+              ah2[mt][0] = hv2.x; ah2[mt][1] = hv2.y; ah2[mt][2] = hv2.z; ah2[mt][3] = hv2.w;
+              al2[mt][0] = lv2.x; al2[mt][1] = lv2.y; al2[mt][2] = lv2.z; al2[mt][3] = lv2.w;
             }
           }
-        }
-      }
-    };
-    if (rowloc) mma_loop(std::true_type{});
-    else mma_loop(std::false_type{});
-    // outputs: m-tile mt, rows g (+8 h); group q: columns cl + 16 q .. + 3 =
-    // (n-tile 2q: c0, c1 | n-tile 2q+1: c0, c1) for row g, (c2, c3 | c2, c3) for row g + 8
 #pragma unroll
-    for (int mt = 0; mt < 2; mt++)
+          for (int nt = 0; nt < 4; nt++) {
+            const size_t o = ((size_t)(ntb + nt) * KS + ks) * 32 + lane;
+            const uint4 b = qs[o];
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int i = 32 * wr + 16 * mt + g + 8 * h;
-        if (i >= nr) continue;
-#pragma unroll
-        for (int q = 0; q < 2; q++) {
-          const int j = cl + 16 * q;
-          if (j >= nc) continue;
-          float mr[4] = {ds[mt][2 * q][2 * h], ds[mt][2 * q][2 * h + 1], ds[mt][2 * q + 1][2 * h],
-                         ds[mt][2 * q + 1][2 * h + 1]};
-          if (rbf) {
-#pragma unroll
-            for (int z = 0; z < 4; z++) mr[z] = __bfloat162float(__float2bfloat16_rn(mr[z]));
-          }
-          const size_t row = (size_t)(R0 + i), col = (size_t)(C0 + j);
-          if (p.recon) {
-            if (rbf) {
-              __nv_bfloat162 b01 = __floats2bfloat162_rn(mr[0], mr[1]), b23 = __floats2bfloat162_rn(mr[2], mr[3]);
-              uint2 raw;
-              raw.x = *reinterpret_cast<unsigned*>(&b01);
-              raw.y = *reinterpret_cast<unsigned*>(&b23);
-              *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + row * p.ldr + col) = raw;
-            } else {
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.recon) + row * p.ldr + col) =
-                  make_float4(mr[0], mr[1], mr[2], mr[3]);
-            }
-          }
-          if (p.err_out) {
-            const float4 a = val<MBF>(av[mt][h][q]);
-            float4 e;
+            for (int mt = 0; mt < 2; mt++) mma3x(ds[mt][nt], ah[mt], al[mt], b.x, b.y, b.z, b.w);
             if (DPL) {
-              e = make_float4(a.x - dw[mt][2 * q][2 * h], a.y - dw[mt][2 * q][2 * h + 1], a.z - dw[mt][2 * q + 1][2 * h],
-                              a.w - dw[mt][2 * q + 1][2 * h + 1]);
-            } else {
-              e = make_float4(a.x - mr[0], a.y - mr[1], a.z - mr[2], a.w - mr[3]);
+              if (OT) {
+#pragma unroll
+                for (int mt = 0; mt < 2; mt++) mma3x(dw[mt][nt], ah2[mt], al2[mt], b.x, b.y, b.z, b.w);
+              } else {
+                const uint4 bw = qw[o];
+#pragma unroll
+                for (int mt = 0; mt < 2; mt++) mma3x(dw[mt][nt], ah[mt], al[mt], bw.x, bw.y, bw.z, bw.w);
+              }
             }
-            *reinterpret_cast<float4*>(p.err_out + row * p.lde_out + col) = e;
           }
         }
-      }
+      };
+      if (rowloc) mma_loop(std::true_type{});
+      else mma_loop(std::false_type{});
+      // outputs: m-tile mt, rows g (+8 h); group q: columns 64 hf + cl + 16 q .. + 3 =
+      // (n-tile 2q: c0, c1 | n-tile 2q+1: c0, c1) for row g, (c2, c3 | c2, c3) for row g + 8
+#pragma unroll
+      for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int i = 32 * wr + 16 * mt + g + 8 * h;
+          if (i >= nr) continue;
+#pragma unroll
+          for (int q = 0; q < 2; q++) {
+            const int j = 64 * hf + cl + 16 * q;
+            if (j >= nc) continue;
+            float mr[4] = {ds[mt][2 * q][2 * h], ds[mt][2 * q][2 * h + 1], ds[mt][2 * q + 1][2 * h],
+                           ds[mt][2 * q + 1][2 * h + 1]};
+            if (rbf) {
+#pragma unroll
+              for (int z = 0; z < 4; z++) mr[z] = __bfloat162float(__float2bfloat16_rn(mr[z]));
+            }
+            const size_t row = (size_t)(R0 + i), col = (size_t)(C0 + j);
+            if (p.recon) {
+              if (rbf) {
+                __nv_bfloat162 b01 = __floats2bfloat162_rn(mr[0], mr[1]), b23 = __floats2bfloat162_rn(mr[2], mr[3]);
+                uint2 raw;
+                raw.x = *reinterpret_cast<unsigned*>(&b01);
+                raw.y = *reinterpret_cast<unsigned*>(&b23);
+                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.recon) + row * p.ldr + col) = raw;
+              } else {
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.recon) + row * p.ldr + col) =
+                    make_float4(mr[0], mr[1], mr[2], mr[3]);
+              }
+            }
+            if (p.err_out) {
+              const float4 a = val<MBF>(av[mt][h][q]);
+              float4 e;
+              if (DPL) {
+                e = make_float4(a.x - dw[mt][2 * q][2 * h], a.y - dw[mt][2 * q][2 * h + 1],
+                                a.z - dw[mt][2 * q + 1][2 * h], a.w - dw[mt][2 * q + 1][2 * h + 1]);
+              } else {
+                e = make_float4(a.x - mr[0], a.y - mr[1], a.z - mr[2], a.w - mr[3]);
+              }
+              *reinterpret_cast<float4*>(p.err_out + row * p.lde_out + col) = e;
+            }
+          }
+        }
+    }
   }
 }
 

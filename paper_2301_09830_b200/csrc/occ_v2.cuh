@@ -47,7 +47,7 @@ constexpr int NT = 512;
 constexpr int NW = 16;
 constexpr int NCW = NW - 1;     // compute warps; warp NW-1 is the phase-1 copy producer
 constexpr int SR = 8;           // tile rows per staging stage (one cell row block)
-constexpr int MAX_STAGES = 4;
+constexpr int MAX_STAGES = 6;
 constexpr int TMEM_CELLS = 512 / (NW / 4) / 4;  // cells per warp in TMEM (its columns / 4)
 constexpr int kTrStamps = 24;   // per-CTA phase-trace stamps (occ_read_trace)
 
