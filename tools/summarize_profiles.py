@@ -58,33 +58,80 @@ def ncu_full(rep):
     return None
 
 
+def ncu_kernels(rep, match):
+    """Key metrics of every captured kernel whose name contains `match`."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    if not rows:
+        return []
+    h = rows[0]
+    out = []
+    for r in rows[2:]:
+        d = dict(zip(h, r))
+        if match in d.get("Kernel Name", ""):
+            x = {"kernel": d["Kernel Name"]}
+            for k in METRICS + ["sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+                                "smsp__average_warp_latency_per_inst_issued.ratio"]:
+                v = d.get(k)
+                try:
+                    x[k] = float(v.replace(",", "")) if v not in (None, "") else None
+                except ValueError:
+                    x[k] = v
+            out.append(x)
+    return out
+
+
 def main():
-    tag = sys.argv[1] if len(sys.argv) > 1 else "round1"
+    tag = sys.argv[1] if len(sys.argv) > 1 else "round2"
+    pre = os.path.join(RAW, "r2f")
     os.makedirs(OUT, exist_ok=True)
-    b1 = last_json(os.path.join(RAW, "bench_n1.json"))
-    json.dump(b1, open(os.path.join(OUT, f"{tag}_bench_n1.json"), "w"), indent=1)
-    ref = os.path.join(RAW, "bench_ref.json")
-    if os.path.exists(ref):
-        json.dump(last_json(ref), open(os.path.join(OUT, f"{tag}_bench_reference.json"), "w"), indent=1)
-    ll = launches(os.path.join(RAW, "launches_n1.csv"))
-    with open(os.path.join(OUT, f"{tag}_launches_n1.csv"), "w") as f:
-        w = csv.writer(f)
-        w.writerow(["kernel", "launches", "mean_us", "share_of_listed_time"])
-        for x in ll:
-            w.writerow([x["kernel"], x["launches"], x["mean_us"], x["share_of_listed_time"]])
-    full = ncu_full(os.path.join(RAW, "prof_bench_n1.ncu-rep"))
-    if full:
-        full["source"] = ("ncu --set full --clock-control none --import-source on -k regex:occ_v2 --launch-skip 3 -c 1 "
-                          "python bench.py --steps 5 --warmup 3 (tools/round_profile.sh)")
-        json.dump(full, open(os.path.join(OUT, f"{tag}_ncu_full_v2_n1.json"), "w"), indent=1)
-        cfg = b1["config"]
-        key = f"{cfg['n']}x{cfg['m']}x{cfg['rank']}"
-        traffic = {key: int((full["dram__bytes_read.sum"] + full["dram__bytes_write.sum"]) * 1e6),
+    res = {}
+    for name in ("bench_n1", "bench_C3", "bench_C4", "bench_ref"):
+        f = f"{pre}_{name}.json"
+        if os.path.exists(f):
+            try:
+                d = last_json(f)
+            except Exception:
+                continue
+            json.dump(d, open(os.path.join(OUT, f"{tag}_{name.replace('bench_ref', 'bench_reference')}.json"), "w"),
+                      indent=1)
+            res[name] = d.get("ms_per_step")
+    f = f"{pre}_launches_n1.csv"
+    if os.path.exists(f):
+        ll = launches(f)
+        with open(os.path.join(OUT, f"{tag}_launches_n1.csv"), "w") as fo:
+            w = csv.writer(fo)
+            w.writerow(["kernel", "launches", "mean_us", "share_of_listed_time"])
+            for x in ll:
+                w.writerow([x["kernel"], x["launches"], x["mean_us"], x["share_of_listed_time"]])
+        res["launches"] = ll[:4]
+    caps = {"v2_C2": ("occ_v2_kernel", "bench.py --config C2"), "v2_T": ("occ_v2_kernel", "bench.py --config T"),
+            "phaseA_C3": ("occ_step_kernel", "big_phase_times multi, launch 0"),
+            "phaseD_C3": ("occ_step_kernel", "big_phase_times multi, launch 5"),
+            "decompress_C3": ("occ_v2_decompress_band", "big_phase_times multi, EF + plain"),
+            "phaseF_C4": ("occ_step_kernel", "big_phase_times multi, launch 30 (DP reconstruction, MLP)")}
+    ncu = {}
+    for key, (match, how) in caps.items():
+        rep = f"{pre}_{key}.ncu-rep"
+        if os.path.exists(rep):
+            ncu[key] = {"source": f"ncu --set full --clock-control none --import-source on ({how}); tools/round2_profile.sh",
+                        "kernels": ncu_kernels(rep, match)}
+    json.dump(ncu, open(os.path.join(OUT, f"{tag}_ncu_full.json"), "w"), indent=1)
+    if "v2_C2" in ncu and ncu["v2_C2"]["kernels"]:
+        k = ncu["v2_C2"]["kernels"][0]
+        traffic = {"C2": int((k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]) * 1e6),
                    "_note": ("dram__bytes_read.sum + dram__bytes_write.sum (MB in the ncu report) of the fused "
-                             f"kernel from profiles/{tag}_ncu_full_v2_n1.json. Writes of e_new/M' still resident in L2 "
-                             "at kernel end are written back after the kernel and are not counted.")}
+                             f"kernel on C2 from profiles/{tag}_ncu_full.json (ncu flushes caches before the "
+                             "replayed kernel; writes still in L2 at kernel end are not counted).")}
+        if "v2_T" in ncu and ncu["v2_T"]["kernels"]:
+            kt = ncu["v2_T"]["kernels"][0]
+            traffic["T"] = int((kt["dram__bytes_read.sum"] + kt["dram__bytes_write.sum"]) * 1e6)
         json.dump(traffic, open(os.path.join(OUT, "traffic.json"), "w"), indent=1)
-    print(json.dumps({"bench": b1["ms_per_step"], "launches": ll[:3], "ncu": full}, indent=1))
+    f = f"{pre}_rank_sweep.jsonl"
+    if os.path.exists(f):
+        with open(os.path.join(OUT, f"{tag}_rank_sweep.jsonl"), "w") as fo:
+            fo.write("".join(x for x in open(f) if x.startswith("{")))
+    print(json.dumps(res, indent=1))
 
 
 if __name__ == "__main__":
