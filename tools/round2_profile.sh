@@ -34,3 +34,11 @@ python tools/big_phase_times.py multi > /dev/null 2>&1 && {
 }
 timeout 600 python tools/rank_sweep.py > ${o}_rank_sweep.jsonl 2> ${o}_rank_sweep.err
 echo "rank sweep rc=$?"
+# gpurun brings back at most 64 MiB: keep the raw metric pages (CSV) of every
+# capture and only the C2 report itself (source-level view)
+for rep in ${o}_*.ncu-rep; do
+  ncu -i $rep --page raw --csv > ${rep%.ncu-rep}.raw.csv 2>/dev/null
+  ncu -i $rep --page details --csv > ${rep%.ncu-rep}.details.csv 2>/dev/null
+  case $rep in *_v2_C2.ncu-rep) ;; *) rm -f $rep ;; esac
+done
+ls -la gpurun_out | tail -40

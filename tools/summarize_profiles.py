@@ -59,8 +59,15 @@ def ncu_full(rep):
 
 
 def ncu_kernels(rep, match):
-    """Key metrics of every captured kernel whose name contains `match`."""
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """Key metrics of every captured kernel whose name contains `match` (from the
+    report, or from its raw-page CSV exported on the GPU box)."""
+    csvp = rep[:-len(".ncu-rep")] + ".raw.csv"
+    if os.path.exists(csvp):
+        raw = open(csvp).read()
+    elif os.path.exists(rep):
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    else:
+        return []
     rows = list(csv.reader(io.StringIO(raw)))
     if not rows:
         return []
@@ -113,7 +120,7 @@ def main():
     ncu = {}
     for key, (match, how) in caps.items():
         rep = f"{pre}_{key}.ncu-rep"
-        if os.path.exists(rep):
+        if os.path.exists(rep) or os.path.exists(f"{pre}_{key}.raw.csv"):
             ncu[key] = {"source": f"ncu --set full --clock-control none --import-source on ({how}); tools/round2_profile.sh",
                         "kernels": ncu_kernels(rep, match)}
     json.dump(ncu, open(os.path.join(OUT, f"{tag}_ncu_full.json"), "w"), indent=1)
