@@ -188,6 +188,31 @@ class ThreeDStep:
         if record is not None:
             record["emb_compressed"] = comp
 
+    # -------------------------------------------------------------- checkpoint / resume
+    def state_dict(self) -> Dict:
+        """The compression state a resumed run needs: the lazy
+        error and warm-start factor of the backward link, the DP error-feedback
+        buffers and factors, and the embedding's; tensors are copied."""
+        st = {}
+        if self.send:
+            st["link.e"], st["link.Q"] = self.e.clone(), self.Q.clone()
+        for j, d in enumerate(self.dp_state):
+            st[f"dp.{j}.e"], st[f"dp.{j}.Q"] = d["e"].clone(), d["Q"].clone()
+        if self.stage in (0, self.P - 1):
+            st["emb.e"], st["emb.Q"] = self.emb_e.clone(), self.emb_Q.clone()
+        return st
+
+    def load_state_dict(self, st: Dict):
+        if self.send:
+            self.e.copy_(st["link.e"])
+            self.Q.copy_(st["link.Q"])
+        for j, d in enumerate(self.dp_state):
+            d["e"].copy_(st[f"dp.{j}.e"])
+            d["Q"].copy_(st[f"dp.{j}.Q"])
+        if self.stage in (0, self.P - 1):
+            self.emb_e.copy_(st["emb.e"])
+            self.emb_Q.copy_(st["emb.Q"])
+
     def close(self):
         if self.link is not None:
             self.link.close()

@@ -73,7 +73,10 @@ def main():
     step = threed.ThreeDStep(policy, P, D, comm, SH, dev, use_link=use_link, init_q=init_q)
     stage, rep = step.stage, step.replica
     records = []
+    saved = None
     for it in range(ITERS):
+        if it == ITERS - 1:
+            saved = step.state_dict()   # checkpoint before the last iteration (replayed below)
         rec = {}
         step.backward_sends(it, lambda k: torch.from_numpy(act(it, stage, rep, k)).to(dev), record=rec)
         Ws = [torch.from_numpy(weight(it, rank, j)).to(dev) for j in range(len(SH.weights))]
@@ -88,9 +91,31 @@ def main():
         rec["G"] = G.double().cpu().numpy() if G is not None else None
         rec["recv"] = [(k, c, o.double().cpu().numpy()) for k, c, o in rec.get("recv", [])]
         records.append(rec)
+    # resume: restore the checkpoint and replay the last iteration; every output must repeat bit for bit
+    step.load_state_dict(saved)
+    it = ITERS - 1
+    rec2 = {}
+    step.backward_sends(it, lambda k: torch.from_numpy(act(it, stage, rep, k)).to(dev), record=rec2)
+    Ws = [torch.from_numpy(weight(it, rank, j)).to(dev) for j in range(len(SH.weights))]
+    Vs = [torch.from_numpy(vector(it, rank, j)).to(dev) for j in range(len(SH.vectors))]
+    step.dp_sync(it, Ws, Vs)
+    G = torch.from_numpy(emb(it, rank, stage)).to(dev) if stage in (0, P - 1) else None
+    if G is not None:
+        step.embedding_sync(it, G)
+    torch.cuda.synchronize()
+    same = all(np.array_equal(w.double().cpu().numpy(), records[it]["W"][j]) for j, w in enumerate(Ws))
+    same = same and (G is None or np.array_equal(G.double().cpu().numpy(), records[it]["G"]))
+    same = same and all(np.array_equal(o.double().cpu().numpy(), r[2])
+                        for (_, _, o), r in zip(rec2.get("recv", []), records[it]["recv"]))
+    same_t = torch.tensor([1 if same else 0], device=dev)
+    dist.all_reduce(same_t, op=dist.ReduceOp.MIN)
     occ.occ_check_status(comm=comm)
     ok = True
     if rank == 0:
+        x = {"check": "threed_checkpoint_resume", "bit_identical_replay": bool(same_t.item()), "ok": bool(same_t.item()),
+             "world": world, "exchange": "link" if use_link else "nccl"}
+        print(json.dumps(x), flush=True)
+        ok = ok and x["ok"]
         out = []
         # (1) the backward link into stage 0, replica 0: the sender is stage 1, replica 0
         e = np.zeros((SH.act_rows, SH.hidden))
