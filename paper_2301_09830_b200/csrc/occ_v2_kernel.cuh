@@ -93,6 +93,8 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   // bulk copy per row and matrix, issued by 2 SR lanes of the producer warp in
   // one instruction (a single issuing thread caps a CTA at ~40 GB/s of 2 KB copies)
   const unsigned long long pol_ef = l2_evict_first();
+  // stores: evict-first by default; OCC_V2_DEBUG bit 1024: the normal policy (experiment)
+  const unsigned long long pol_st = (p.debug & 1024) ? l2_evict_normal() : pol_ef;
   auto issue = [&](int s) {
     const int slot = s % p.ns;
     const int r0 = s * SR, nrow = min(SR, T.th - r0);
@@ -522,16 +524,16 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
                 if (HASR) {
                   if (MBF) {
                     const __nv_bfloat162 b0 = __floats2bfloat162_rn(mr[0], mr[2]), b1 = __floats2bfloat162_rn(mr[1], mr[3]);
-                    st_b32_hint(rp + ro, *reinterpret_cast<const unsigned*>(&b0), pol_ef);
-                    st_b32_hint(rp + ro + r4, *reinterpret_cast<const unsigned*>(&b1), pol_ef);
+                    st_b32_hint(rp + ro, *reinterpret_cast<const unsigned*>(&b0), pol_st);
+                    st_b32_hint(rp + ro + r4, *reinterpret_cast<const unsigned*>(&b1), pol_st);
                   } else {
-                    st_f2_hint(reinterpret_cast<float*>(rp + ro), make_float2(mr[0], mr[2]), pol_ef);
-                    st_f2_hint(reinterpret_cast<float*>(rp + ro + r4), make_float2(mr[1], mr[3]), pol_ef);
+                    st_f2_hint(reinterpret_cast<float*>(rp + ro), make_float2(mr[0], mr[2]), pol_st);
+                    st_f2_hint(reinterpret_cast<float*>(rp + ro + r4), make_float2(mr[1], mr[3]), pol_st);
                   }
                 }
                 if (HASE) {
-                  st_f2_hint(ep + eo, sub2(make_float2(v[0], v[2]), make_float2(mr[0], mr[2])), pol_ef);
-                  st_f2_hint(ep + eo + e4, sub2(make_float2(v[1], v[3]), make_float2(mr[1], mr[3])), pol_ef);
+                  st_f2_hint(ep + eo, sub2(make_float2(v[0], v[2]), make_float2(mr[0], mr[2])), pol_st);
+                  st_f2_hint(ep + eo + e4, sub2(make_float2(v[1], v[3]), make_float2(mr[1], mr[3])), pol_st);
                 }
               } else {
                 store_cell_edge<MBF>(p, T, 8 * rblk + t, c, make_float4(mr[0], mr[1], mr[2], mr[3]),
