@@ -15,7 +15,7 @@ template <int R>
 __host__ __device__ constexpr size_t orth_bytes() { return (sizeof(OrthSmem<R>) + 15) / 16 * 16; }
 
 template <int R, bool DPL>
-__global__ void __launch_bounds__(NT, (R <= 16) ? 2 : 1) occ_step_kernel(Params p, int ph0, int ph1, int coop) {
+__global__ void __launch_bounds__(NT, 1) occ_step_kernel(const __grid_constant__ Params p, int ph0, int ph1, int coop) {
   extern __shared__ __align__(16) unsigned char smraw[];
   float* sm = reinterpret_cast<float*>(smraw);
   unsigned nb = 0;
@@ -262,7 +262,7 @@ cudaError_t run_phases(const Params& p, const Geometry& g, int ph0, int ph1, boo
 // ------------------------------------------------------------------ decompress
 // out = round(P Q^T): a standalone phase F with no residual (receiver side).
 template <int R>
-__global__ void __launch_bounds__(NT) occ_decompress_kernel(Params p) {
+__global__ void __launch_bounds__(NT) occ_decompress_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(16) unsigned char smraw[];
   phase_F<R, false>(p, reinterpret_cast<float*>(smraw));
 }
