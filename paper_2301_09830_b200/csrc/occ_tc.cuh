@@ -93,7 +93,7 @@ struct TcCfg {
   static constexpr int NTL = (R + 7) / 8;     // n-tiles of 8 over the rank (R = 4: one, half zero)
   static constexpr int A_ROWS = 16 * NW;      // phase A: rows per unit (one m-tile per warp)
   static constexpr int D_COLS = 32 * NW;      // phase D: columns per unit (two m-tiles per warp)
-  static constexpr int PD = (R <= 16) ? 3 : 4;   // steps of raw loads in flight per warp (R >= 32: one CTA per SM)
+  static constexpr int PD = (R <= 16) ? 4 : 6;   // steps of raw loads in flight per warp (one CTA of 8 warps per SM)
 };
 
 // shared memory of phase A for a split of width cs1: the Q slab fragments
