@@ -719,7 +719,12 @@ cudaError_t run_link_exchange(const float* sP, const float* sQ, float* pP, float
                               cudaStream_t st) {
   // a few CTAs: the transfer is small and every CTA pays a system-scope fence
   const long long vec = std::max(nP + nQ, mnP + mnQ) / 4;
-  const int grid = (int)std::max<long long>(1, std::min<long long>(32, (vec + 1023) / 1024));
+  static const int cap = [] {   // OCC_LINK_GRID: CTA cap of the link copies (experiment), default 32
+    const char* e = getenv("OCC_LINK_GRID");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 32;
+  }();
+  const int grid = (int)std::max<long long>(1, std::min<long long>(cap, (vec + 1023) / 1024));
   v2::occ_link_exchange_kernel<<<grid, 256, 0, st>>>(sP, sQ, pP, pQ, nP, nQ, ack_in, push_ctr, peer_flag, sseq, mP, mQ,
                                                      dP, dQ, mnP, mnQ, flag_in, recv_ctr, peer_ack, rseq);
   return cudaGetLastError();
