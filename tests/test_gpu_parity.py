@@ -633,3 +633,27 @@ def test_dp_orient_t_single_rank_matches_oracle(flags, r):
         assert rel(Qd.double().cpu().numpy(), o["Q"], o["Q"]) <= 1e-3
     finally:
         comm.destroy()
+
+
+def test_dp_mixed_shape_bucket_matches_oracle():
+    """A DP bucket of matrices with different shapes (each matrix's
+    sweep-1 partials need s1_i n_i rows, which can exceed those of the largest
+    shape): the advisor's (3581, 304) + (4861, 184) at r = 64, and the C4
+    shapes' aspect, each against the oracle's dp_step (1-rank group)."""
+    r = 64
+    shapes = [(3576, 304), (4856, 184), (512, 2048)]   # rows x cols (cols % 8 == 0)
+    Ms = [synth.d2_gradlike(a, b, 181 + i) for i, (a, b) in enumerate(shapes)]
+    Es = [synth.e0(a, b, 191 + i, like=Ms[i]) for i, (a, b) in enumerate(shapes)]
+    Q0s = [synth.q0(b, r, 201 + i) for i, (_, b) in enumerate(shapes)]
+    Gd = [to_dev(x) for x in Ms]
+    Ed = [to_dev(x) for x in Es]
+    Qd = [to_dev(x) for x in Q0s]
+    Pd = [torch.empty(a, r, device="cuda") for a, _ in shapes]
+    occ.occ_allreduce_factors(Gd, Ed, Qd, Pd, r, 1.0)
+    torch.cuda.synchronize()
+    for i in range(len(shapes)):
+        o = oracle.dp_step([Ms[i]], [Es[i]], Q0s[i], scale=1.0)
+        A = Ms[i].astype(np.float64) + Es[i]
+        G = Gd[i].double().cpu().numpy()
+        assert rel(G, o["recon"], A) <= TOL32 and elem(G, o["recon"], A) <= TOL32 / 10, i
+        assert rel(Ed[i].double().cpu().numpy(), o["err"][0], A) <= TOL32, i
