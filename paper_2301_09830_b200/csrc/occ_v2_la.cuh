@@ -30,7 +30,7 @@ struct OrthW {  // small fp64 linear algebra in shared memory
   double dinv[32];      // D^-1/2
   int rep[32];
   int deg;
-  int prog;             // ldl_warp progress (publish mode): steps done; R + 1 = finished; -1 = degenerate
+  int prog;             // R + 2: Li, kappa, amp ready; -1: degenerate column (phase 3 protocol)
   double kappa;
   double amp;           // ||S Li^T||_F, S = diag(||p_j||): error amplification of Q = (A^T P) Li^T
 };
@@ -148,14 +148,14 @@ __device__ __forceinline__ int prog_acquire(const OrthW& o) {
 // stop at the first column whose squared residual D_j is below tau2 * its own
 // squared norm (reading C3: the MGS test ||v|| < tau ||p_j||) and return 1 (o.L
 // is then partially overwritten; callers re-reduce it).  publish: advance o.prog
-// after every column, so solve_rows_pipelined can trail one step behind.
+// after every column (kept for experiments; the hot path uses the unrolled form).
 template <int R>
 __device__ int ldl_warp(OrthW& o, double tau2, bool detect, bool publish = false) {
   const int i = threadIdx.x & 31;
   double rr[R];
 #pragma unroll
   for (int k = 0; k < R; k++) rr[k] = (i < R) ? o.L[i * LD + k] : 0.0;
-  if (publish && R <= 16) {   // rows R..31 of o.L read as zero by solve_rows_pipelined
+  if (publish && R <= 16) {   // rows R..31 of o.L read as zero by a row solver trailing the factorisation
     for (int x = i; x < (32 - R) * LD; x += 32) o.L[R * LD + x] = 0.0;
   }
   int deg = 0;
@@ -239,7 +239,8 @@ __device__ void inverse_warp(OrthW& o) {
 // The same factorisation fully unrolled (register rows, static indices): the
 // dynamic instruction count is ~35% lower than the rotated loop's (3.9k vs
 // 6.0k cycles for R = 16, tools/la_bench.cu), at ~1.2k more instructions of
-// code.  Used on the hot path, always in publish mode; same protocol and
+// code.  Used on the hot path (publishes only a degenerate column; Li, kappa
+// and amp are published by inverse_warp_unrolled); same
 // results as ldl_warp.
 template <int R>
 __device__ int ldl_warp_unrolled(OrthW& o, double tau2, bool detect) {
@@ -247,9 +248,6 @@ __device__ int ldl_warp_unrolled(OrthW& o, double tau2, bool detect) {
   double row[R];
 #pragma unroll
   for (int k = 0; k < R; k++) row[k] = (i < R) ? o.L[i * LD + k] : 0.0;
-  if (R <= 16) {   // rows R..31 of o.L read as zero by solve_rows_pipelined
-    for (int x = i; x < (32 - R) * LD; x += 32) o.L[R * LD + x] = 0.0;
-  }
   int deg = 0;
 #pragma unroll
   for (int j = 0; j < R; j++) {
@@ -268,8 +266,7 @@ __device__ int ldl_warp_unrolled(OrthW& o, double tau2, bool detect) {
       o.L[i * LD + j] = lij;
     }
     if (i == j) { o.D[j] = d; row[j] = 1.0; }
-    __syncwarp();
-    if (i == 0) prog_release(o, j + 1);
+    __syncwarp();   // (no per-step publish: the other warps wait for Li, o.prog = R + 2)
   }
   if (!deg && i < R) {
 #pragma unroll
@@ -277,7 +274,7 @@ __device__ int ldl_warp_unrolled(OrthW& o, double tau2, bool detect) {
     o.dinv[i] = 1.0 / sqrt(o.D[i]);
   }
   __syncwarp();
-  if (i == 0) prog_release(o, deg ? -1 : R + 1);
+  if (deg && i == 0) prog_release(o, -1);
   return deg;
 }
 
@@ -433,89 +430,6 @@ __device__ void band_solve(const float* ps, float* out, int nr, const OrthW& o, 
     }
 #pragma unroll
     for (int a = 0; a < R; a++) out[i * RP + a] = (float)(x[a] * o.dinv[a]);
-  }
-}
-
-// Fused path (reading C20), pipelined behind ldl_warp(publish): every row x of
-// src ([nrows][ld]; rows >= nvalid zero) becomes D^-1/2 L^-1 x (-> dst [.][dld])
-// by right-looking substitution: at step a, x_a is final once column a of L is
-// (o.prog > a), and x_{a+k} -= l_{a+k,a} x_a.  The registers are shifted like
-// ldl_warp's: xr[k] holds x_{a+k}; the finished x_a enters at xr[R-1] and
-// shifts left with the rest (its l is 0: rows R.. of o.L are zero), so after R
-// steps xr[k] = x_k.  One row per thread x of the calling group (nthr threads).
-// Returns false (writes nothing) if the factorisation stopped at a degenerate
-// column.
-template <int R>
-__device__ __forceinline__ bool solve_rows_pipelined(const float* src, int ld, int nrows, int nvalid, float* dst,
-                                                     int dld, const OrthW& o, int x, int nthr) {
-  bool ok = true;
-  int seen = 0;
-  for (int it = x; it < nrows; it += nthr) {
-    const float* s = src + (size_t)it * ld;
-    const bool zero = it >= nvalid;
-    double xr[R];
-#pragma unroll
-    for (int k = 0; k < R; k++) xr[k] = zero ? 0.0 : (double)s[k];
-    // column a of L (from the diagonal down) is loaded during step a - 1 when
-    // the factorisation is already past it, so the loads' latency overlaps the
-    // previous step's FMAs instead of sitting in front of each FMA
-    auto load_col = [&](int a, double (&lv)[R - 1]) {
-      const double* la = o.L + a * (LD + 1);
-#pragma unroll
-      for (int k = 1; k < R; k++) lv[k - 1] = (R <= 16 || a + k < 32) ? la[k * LD] : 0.0;
-    };
-    double lv[R - 1];
-    bool have = false;
-#pragma unroll 1
-    for (int a = 0; a < R; a++) {
-      if (!have) {
-        if (!wait_prog(o, a + 1, seen)) { ok = false; break; }
-        load_col(a, lv);
-      }
-      const double xa = xr[0];
-      double cur[R - 1];
-#pragma unroll
-      for (int k = 0; k < R - 1; k++) cur[k] = lv[k];
-      have = a + 1 < R && seen >= a + 2;   // next column already final: prefetch it now
-      if (have) load_col(a + 1, lv);
-#pragma unroll
-      for (int k = 1; k < R; k++) xr[k - 1] = fma(-cur[k - 1], xa, xr[k]);
-      xr[R - 1] = xa;
-    }
-    if (!ok || !wait_prog(o, R + 1, seen)) { ok = false; break; }
-    float* d = dst + (size_t)it * dld;
-#pragma unroll
-    for (int k = 0; k < R; k++) d[k] = (float)(xr[k] * o.dinv[k]);
-  }
-  return ok && wait_prog(o, R + 1, seen);
-}
-
-// Fused path (reading C20): rows x -> D^-1/2 L^-1 x by forward substitution
-// with the unit lower L of G = L D L^T, for the H8 rows of the P band (rows >= th
-// zero; -> P_hat) and the nqc rows of the reduced Q~ slice (-> Q).  One row per
-// thread of the NCW compute warps; fp64, rounded to fp32.
-template <int R>
-__device__ __forceinline__ void solve_rows(const float* ps, int H8, int th, const float* qt, int nqc, const OrthW& o,
-                                           float* phat, float* qout) {
-  constexpr int RP = K<R>::RP;
-  for (int it = threadIdx.x; it < H8 + nqc; it += NCW * 32) {
-    const bool isP = it < H8;
-    const float* src = isP ? ps + (size_t)it * RP : qt + (size_t)(it - H8) * R;
-    const bool zero = isP && it >= th;
-    double x[R];
-#pragma unroll
-    for (int a = 0; a < R; a++) {
-      double v0 = zero ? 0.0 : (double)src[a], v1 = 0.0;
-#pragma unroll
-      for (int b = 0; b < a; b++) {
-        if (b & 1) v1 = fma(-o.L[a * LD + b], x[b], v1);
-        else v0 = fma(-o.L[a * LD + b], x[b], v0);
-      }
-      x[a] = v0 + v1;
-    }
-    float* dst = isP ? phat + (size_t)it * RP : qout + (size_t)(it - H8) * R;
-#pragma unroll
-    for (int a = 0; a < R; a++) dst[a] = (float)(x[a] * o.dinv[a]);
   }
 }
 
