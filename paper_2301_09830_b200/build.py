@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libocc.so")
 LIB_TRACE = os.path.join(HERE, "libocc_trace.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("occ_api.cu", "occ_step.cu", "occ_v2.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("occ_api.cu", "occ_step.cu", "occ_v2.cu", "occ_umma.cu")]
 DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + \
     glob.glob(os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "occ.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -49,6 +49,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Instrumented build only (libocc_trace.so): CTA 0 stamps an otherwise unused
+// DevStats::t_ns slot inside the per-phase orthonormalisation (tools/orth_times.py).
+#ifdef OCC_TRACE
+#define OCC_STAMP(p, k) \
+  do { if (blockIdx.x == 0 && threadIdx.x == 0) (p).stats->t_ns[k] = gtimer(); } while (0)
+#else
+#define OCC_STAMP(p, k) do { } while (0)
+#endif
 
 // Sender side of one occ_link step (include/occ.h): the
 // factors go to slot seq % 2 of the peer's mailbox with NVLink stores, then
@@ -135,6 +143,7 @@ struct Params {
   int path;
   int f_tc;              // phase F on the tensor cores (occ_tc.cuh phase_F_tc; the DP paths)
   LinkPush push;         // occ_link sender: the fused kernel pushes the factors itself
+  float* Qt;             // workspace: the small factor transposed and split hi / lo (occ_umma.cu)
 };
 
 // ------------------------------------------------------------------ helpers
@@ -608,9 +617,11 @@ __device__ int phase_C1(const Params& p, OrthSmem<R>& o, float* ps) {
   const double tau2 = p.tau * p.tau;
   reduce_gram<R>(p.G_part, p.ngp, o.S);
   __syncthreads();
+  OCC_STAMP(p, 1);
   if (p.check_finite && blockIdx.x == 0 && threadIdx.x < R && !isfinite(o.S[threadIdx.x * R + threadIdx.x]))
     atomicOr(&g_nonfinite_v1, 1u);
   const int deg = chol_inplace<R>(o.S, o.gdiag, tau2, true, &o.flag);
+  OCC_STAMP(p, 2);
   if (deg) {
     // X = P^T F, Y = F^T F partials for this CTA's rows
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -634,12 +645,14 @@ __device__ int phase_C1(const Params& p, OrthSmem<R>& o, float* ps) {
     return 2;
   }
   tri_inverse<R>(o.S, o.Li, &o.kappa);
+  OCC_STAMP(p, 4);
   const bool need2 = p.force_two_pass || o.kappa > p.kappa_thr;
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
     apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, false, p.fb_seed, ps, o.X);
     if (need2) gram_partial<R>(p.P, r0, nr, p.G2_part + (size_t)u * npairs(R), ps);
   }
+  OCC_STAMP(p, 5);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p.ctl[0] = need2 ? 3 : 0;
     p.stats->fallback_columns = 0;
@@ -687,9 +700,12 @@ __device__ void phase_C3(const Params& p, OrthSmem<R>& o, float* ps) {
   const int units = (p.n + B_ROWS - 1) / B_ROWS;
   reduce_gram<R>(p.G2_part, p.ngp, o.S);
   __syncthreads();
+  OCC_STAMP(p, 9);
   chol_inplace<R>(o.S, o.gdiag, 0.0, false, &o.flag);
+  OCC_STAMP(p, 10);
   double dummy;
   tri_inverse<R>(o.S, o.Li, &dummy);
+  OCC_STAMP(p, 11);
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
     apply_rinv<R>(p.P, p.P, r0, nr, o.Li, o.rep, false, p.fb_seed, ps, o.X);

@@ -179,6 +179,7 @@ WsLayout make_layout(const Geometry& g, int nmat) {
   L.p_bucket = off; off = al(off + (size_t)nmat * g.n * R * 4);
   L.qw_bucket = off; off = al(off + (size_t)nmat * g.m * R * 4);
   L.qs_bucket = off; off = al(off + (size_t)nmat * std::max(g.n, g.m) * R * 4);   // reduced Q (or V, OCC_ORIENT_T)
+  L.qt = off; off = al(off + umma_qt_bytes(g.n, g.m, R));   // tcgen05 sweeps: Q^T / P_hat^T split hi / lo
   L.v2_tail_bytes = v2_tail_bytes(g.n, g.m, R, 148);   // reused by every matrix of a multi-matrix call
   L.v2_tail = off; off = al(off + L.v2_tail_bytes);
   L.total = off;
@@ -195,6 +196,7 @@ void fill_ws(Params& p, const Geometry& g, const WsLayout& L, void* ws) {
   p.G_part = reinterpret_cast<double*>(base + L.g_part);
   p.G2_part = reinterpret_cast<double*>(base + L.g2_part);
   p.XY_part = reinterpret_cast<double*>(base + L.xy_part);
+  p.Qt = reinterpret_cast<float*>(base + L.qt);
   p.s1 = g.s1; p.cs1 = g.cs1; p.s2 = g.s2; p.rs2 = g.rs2; p.ngp = g.ngp;
 }
 
@@ -202,6 +204,17 @@ void fill_ws(Params& p, const Geometry& g, const WsLayout& L, void* ws) {
 // launch (grid = co-resident CTAs); otherwise one launch per phase group.
 template <int R, bool DPL>
 static cudaError_t run_t(Params p, const Geometry& g, int ph0, int ph1, bool multi, cudaStream_t st) {
+  if (ph0 == P_A && ph1 > P_A) {   // sweep 1 on the tcgen05 path (occ_umma.cu) when it applies
+    int G = 0;
+    const cudaError_t eu = run_umma_sweep1(p, R, g.s1, &G, st);
+    if (eu == cudaSuccess) {
+      p.s1 = G;
+      ph0 = P_B1;
+      if (ph0 >= ph1) return cudaSuccess;
+    } else if (eu != cudaErrorNotSupported) {
+      return eu;
+    }
+  }
   auto kern = occ_step_kernel<R, DPL>;
   const size_t smem = smem_bytes_for<R>(g);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
