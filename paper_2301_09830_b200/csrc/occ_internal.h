@@ -24,7 +24,7 @@ constexpr size_t kBarLinesBytes = 8 * 128;                        // (v2::kBarLi
 
 struct WsLayout {
   size_t bar = 0, p_part = 0, q_part = 0, g_part = 0, g2_part = 0, xy_part = 0;
-  size_t p_bucket = 0, qw_bucket = 0, qs_bucket = 0, qt = 0, v2_tail = 0, v2_tail_bytes = 0, total = 0;
+  size_t p_bucket = 0, qw_bucket = 0, qs_bucket = 0, qt = 0, li = 0, v2_tail = 0, v2_tail_bytes = 0, total = 0;
 };
 
 Geometry make_geometry(int64_t n, int64_t m, int r, int sms);
@@ -74,8 +74,12 @@ cudaError_t run_link_exchange(const float* sP, const float* sQ, float* pP, float
                               const unsigned* flag_in, unsigned* recv_ctr, unsigned* peer_ack, unsigned rseq,
                               cudaStream_t st);
 unsigned take_link_timeout();
-// tcgen05 sweep 1 (occ_umma.cu): workspace of the split, transposed small factor
+// tcgen05 sweeps (occ_umma.cu): workspace of the split, transposed small factor
 size_t umma_qt_bytes(int64_t n, int64_t m, int r);
-cudaError_t run_umma_sweep1(const Params& p, int r, int max_splits, int* G_out, cudaStream_t st);
+bool umma_applies(const Params& p, int r);
+// sweep 1 (transposed = false: P_part) or sweep 2 (true: Q_part) on tcgen05
+cudaError_t run_umma_sweep(const Params& p, int r, bool transposed, int max_splits, int* G_out, cudaStream_t st);
+// the DP reconstruction (phase F with f_tc) on tcgen05, r in {32, 64}
+cudaError_t run_umma_recon(const Params& p, int r, cudaStream_t st);
 
 }  // namespace occ

@@ -144,6 +144,8 @@ struct Params {
   int f_tc;              // phase F on the tensor cores (occ_tc.cuh phase_F_tc; the DP paths)
   LinkPush push;         // occ_link sender: the fused kernel pushes the factors itself
   float* Qt;             // workspace: the small factor transposed and split hi / lo (occ_umma.cu)
+  double* Li_g;          // workspace: D^-1/2 L^-1 of the one-CTA factorisation (fast orthonormalisation)
+  int fast_orth;         // per-phase path: one-CTA factorisation between two grid barriers (orth_fast)
 };
 
 // ------------------------------------------------------------------ helpers
@@ -712,6 +714,284 @@ __device__ void phase_C3(const Params& p, OrthSmem<R>& o, float* ps) {
   }
 }
 
+// ------------------------------------------------------------------ fast orthonormalisation
+// The per-phase path's a4 (reading C3, same arithmetic as phases B/C: fp64
+// Gram, LDL^T with the degenerate-column test, L^-1, P_hat = P Li^T in fp64),
+// organised for a cooperative launch so that no CTA repeats another's work:
+//   B  every unit of 128 rows: P = sum of the sweep-1 partials (16-byte
+//      loads, partials in flight together), its fp64 Gram partial with 4 x 4
+//      register blocks
+//   -- grid barrier --
+//   C  CTA 0 alone: the Gram reduce, then ONE right-looking LDL^T sweep that
+//      carries the unit-lower inverse along (Gauss-Jordan on the lower
+//      triangle: row i -= l_ij row j on [S | W], W = I); Li = D^-1/2 W goes to
+//      the workspace, with the plan (0 done, 2 degenerate column, 3 CholQR2)
+//   -- grid barrier --
+//   apply  every CTA: P_hat = P Li^T on its slice of rows (fp64 sums)
+// (the phase_C1 design instead repeated the reduce and the factorisation in
+// all CTAs: 148x the L2 traffic and the slow per-CTA factorisation on the
+// critical path).  A degenerate column falls back to phases C1/C2/C3.
+
+// P[r0 .. r0+nr) = sum_s P_part[s] (16-byte vectors, 4 partials per step in flight)
+template <int R>
+__device__ __forceinline__ void reduce_p_rows(const Params& p, int r0, int nr, float* ps) {
+  const int nv = nr * R / 4;
+  const float4* base = reinterpret_cast<const float4*>(p.P_part + (size_t)r0 * R);
+  const size_t stride = (size_t)p.n * R / 4;
+  for (int x = threadIdx.x; x < nv; x += blockDim.x) {
+    float4 v = __ldcg(base + x);
+    int sidx = 1;
+    for (; sidx + 3 < p.s1; sidx += 4) {
+      const float4 a = __ldcg(base + x + (size_t)sidx * stride), b = __ldcg(base + x + (size_t)(sidx + 1) * stride);
+      const float4 c = __ldcg(base + x + (size_t)(sidx + 2) * stride), d = __ldcg(base + x + (size_t)(sidx + 3) * stride);
+      v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+      v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
+      v.x += c.x; v.y += c.y; v.z += c.z; v.w += c.w;
+      v.x += d.x; v.y += d.y; v.z += d.z; v.w += d.w;
+    }
+    for (; sidx < p.s1; sidx++) {
+      const float4 a = __ldcg(base + x + (size_t)sidx * stride);
+      v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+    }
+    reinterpret_cast<float4*>(p.P + (size_t)r0 * R)[x] = v;
+    if (ps) reinterpret_cast<float4*>(ps)[x] = v;
+  }
+}
+
+// The P reduce alone (phase B1 of a launch that stops before the Gram, the DP
+// path: the P bucket is allreduced next), over every CTA.
+template <int R>
+__device__ void reduce_p_all(const Params& p) {
+  const int rows_per = 8;
+  const int chunks = (p.n + rows_per - 1) / rows_per;
+  for (int c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const int r0 = c * rows_per;
+    reduce_p_rows<R>(p, r0, min(rows_per, p.n - r0), nullptr);
+  }
+}
+
+// Packed upper-triangle Gram of ps[0 .. nr) (fp32 rows) in fp64: 4 x 4 blocks
+// (a0 .. a0+3, b0 .. b0+3), a0 <= b0, each thread one block over a row slice;
+// slices combined through shared memory in a fixed order.
+template <int R>
+__device__ void gram_blocked(const float* ps, int nr, double* out, double* dscr) {
+  constexpr int NB4 = R / 4 < 1 ? 1 : R / 4;
+  constexpr int NBLK = NB4 * (NB4 + 1) / 2;
+  constexpr int RS = (NT / NBLK) < 1 ? 1 : (NT / NBLK);     // row slices
+  constexpr int NP = npairs(R);
+  const int t = threadIdx.x;
+  double g[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; u++)
+#pragma unroll
+    for (int v = 0; v < 4; v++) g[u][v] = 0.0;
+  const int blk = t % NBLK, sl = t / NBLK;
+  int A = 0, rem = blk;
+  while (rem >= NB4 - A) { rem -= NB4 - A; A++; }
+  const int B = A + rem;
+  const bool act = sl < RS && R >= 4;
+  if (act) {
+    const int i0 = (int)((long long)sl * nr / RS), i1 = (int)((long long)(sl + 1) * nr / RS);
+    for (int i = i0; i < i1; i++) {
+      const float4 xa = *reinterpret_cast<const float4*>(ps + i * R + 4 * A);
+      const float4 xb = *reinterpret_cast<const float4*>(ps + i * R + 4 * B);
+      const double a4[4] = {(double)xa.x, (double)xa.y, (double)xa.z, (double)xa.w};
+      const double b4[4] = {(double)xb.x, (double)xb.y, (double)xb.z, (double)xb.w};
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int v = 0; v < 4; v++) g[u][v] = fma(a4[u], b4[v], g[u][v]);
+    }
+  }
+  // combine the row slices: slice 0 adds the others' blocks in slice order
+  if (RS > 1) {
+    if (act && sl > 0) {
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int v = 0; v < 4; v++) dscr[((sl - 1) * NBLK + blk) * 16 + 4 * u + v] = g[u][v];
+    }
+    __syncthreads();
+    if (act && sl == 0) {
+      for (int z = 1; z < RS; z++)
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+          for (int v = 0; v < 4; v++) g[u][v] += dscr[((z - 1) * NBLK + blk) * 16 + 4 * u + v];
+    }
+  }
+  if (act && sl == 0) {
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        const int a = 4 * A + u, b = 4 * B + v;
+        if (a <= b) out[pidx(R, a, b)] = g[u][v];
+      }
+  }
+  if (R < 4 && t < NP) {   // (R < 4 is not instantiated; kept total)
+    int a = 0, rr = t;
+    while (rr >= R - a) { rr -= R - a; a++; }
+    const int b = a + rr;
+    double v = 0.0;
+    for (int i = 0; i < nr; i++) v = fma((double)ps[i * R + a], (double)ps[i * R + b], v);
+    out[t] = v;
+  }
+}
+
+// phase B of the fast orthonormalisation: per 128-row unit, P reduce (or P read)
+// and the fp64 Gram partial into part[u].
+template <int R>
+__device__ void phase_B_fast(const Params& p, const float* src, double* part, bool do_reduce, unsigned char* smraw) {
+  const int units = (p.n + B_ROWS - 1) / B_ROWS;
+  float* ps = reinterpret_cast<float*>(smraw);                                // [B_ROWS][R]
+  double* dscr = reinterpret_cast<double*>(smraw + (size_t)B_ROWS * R * 4);   // slice partials
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
+    __syncthreads();
+    if (do_reduce) {
+      reduce_p_rows<R>(p, r0, nr, ps);
+    } else {
+      for (int x = threadIdx.x; x < nr * R / 4; x += NT)
+        reinterpret_cast<float4*>(ps)[x] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)r0 * R) + x);
+    }
+    __syncthreads();
+    gram_blocked<R>(ps, nr, part + (size_t)u * npairs(R), dscr);
+  }
+}
+
+// CTA 0: Gram reduce + LDL^T with the inverse carried along.  Writes Li =
+// D^-1/2 L^-1 (R x R, lower, row-major) to p.Li_g and returns the plan:
+// 2 a degenerate column (detect), 3 the CholQR2 pass is needed, 0 done.
+template <int R>
+__device__ int factor_fast(const Params& p, const double* part, bool detect, bool first_pass, unsigned char* smraw) {
+  double* S = reinterpret_cast<double*>(smraw);   // [R][R] Gram -> eliminated
+  double* W = S + R * R;                           // [R][R] unit-lower inverse
+  double* gd = W + R * R;                          // [R] Gram diagonal
+  double* red = gd + R;                            // [2][NW] norms
+  int* flag = reinterpret_cast<int*>(red + 2 * NW);
+  constexpr int NP = npairs(R);
+  const double tau2 = p.tau * p.tau;
+  for (int q = threadIdx.x; q < NP; q += NT) {
+    int a = 0, rem = q;
+    while (rem >= R - a) { rem -= R - a; a++; }
+    const int b = a + rem;
+    double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;   // fixed order per entry
+    int u = 0;
+    for (; u + 3 < p.ngp; u += 4) {
+      g0 += __ldcg(part + (size_t)u * NP + q);
+      g1 += __ldcg(part + (size_t)(u + 1) * NP + q);
+      g2 += __ldcg(part + (size_t)(u + 2) * NP + q);
+      g3 += __ldcg(part + (size_t)(u + 3) * NP + q);
+    }
+    for (; u < p.ngp; u++) g0 += __ldcg(part + (size_t)u * NP + q);
+    const double g = (g0 + g1) + (g2 + g3);
+    S[a * R + b] = g;
+    S[b * R + a] = g;
+  }
+  for (int x = threadIdx.x; x < R * R; x += NT) W[x] = (x / R == x % R) ? 1.0 : 0.0;
+  if (threadIdx.x == 0) *flag = 0;
+  __syncthreads();
+  for (int x = threadIdx.x; x < R; x += NT) gd[x] = S[x * R + x];
+  if (first_pass && p.check_finite && threadIdx.x < R && !isfinite(S[threadIdx.x * R + threadIdx.x]))
+    atomicOr(&g_nonfinite_v1, 1u);
+  __syncthreads();
+  for (int j = 0; j < R; j++) {
+    const double d = S[j * R + j], gj = gd[j];
+    if (detect && (gj == 0.0 || !(d >= tau2 * gj))) return 2;   // uniform
+    const double rinv = 1.0 / (d > 0.0 ? d : 1e-300);
+    // rows i > j: S[i][k] -= l_ij S[k][j] (j < k <= i), W[i][k] -= l_ij W[j][k] (k <= j)
+    const int rows = R - 1 - j;
+    for (int x = threadIdx.x; x < rows * R; x += NT) {
+      const int i = j + 1 + x / R, k = x % R;
+      if (k > i) continue;
+      const double l = S[i * R + j] * rinv;
+      if (k > j) S[i * R + k] = fma(-l, S[k * R + j], S[i * R + k]);
+      else W[i * R + k] = fma(-l, W[j * R + k], W[i * R + k]);
+    }
+    __syncthreads();
+  }
+  // Li = D^-1/2 W; kappa_est = ||L D^1/2||_F ||D^-1/2 L^-1||_F
+  double nl = 0.0, ni = 0.0;
+  for (int x = threadIdx.x; x < R * R; x += NT) {
+    const int i = x / R, k = x % R;
+    const double di = S[i * R + i];
+    const double si = 1.0 / sqrt(di > 0.0 ? di : 1e-300);
+    const double li = (k <= i) ? W[x] * si : 0.0;
+    p.Li_g[x] = li;
+    ni = fma(li, li, ni);
+    if (k < i) {
+      const double dk = S[k * R + k];
+      const double lk = S[x] / (dk > 0.0 ? dk : 1e-300);
+      nl = fma(lk * lk, dk, nl);
+    } else if (k == i) {
+      nl += di;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    nl += __shfl_xor_sync(0xffffffffu, nl, off);
+    ni += __shfl_xor_sync(0xffffffffu, ni, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = nl;
+    red[NW + (threadIdx.x >> 5)] = ni;
+  }
+  __syncthreads();
+  int plan = 0;
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < NW; w++) { a += red[w]; b += red[NW + w]; }
+    const double kappa = sqrt(a) * sqrt(b);
+    if (first_pass) {
+      plan = (p.force_two_pass || kappa > p.kappa_thr) ? 3 : 0;
+      p.stats->fallback_columns = 0;
+      p.stats->second_pass = plan == 3 ? 1 : 0;
+      p.stats->kappa_est = kappa;
+    }
+    *flag = plan;
+  }
+  __syncthreads();
+  return *flag;
+}
+
+// every CTA: P_hat = P Li^T on rows [r0, r1) (Li from p.Li_g), chunks of
+// B_ROWS; with gpart (the CholQR2 first pass; r0 on a unit boundary) also the
+// Gram partial of each unit of P_hat.
+template <int R>
+__device__ void apply_fast(const Params& p, int r0, int r1, unsigned char* smraw, double* gpart) {
+  double* Li = reinterpret_cast<double*>(smraw);                            // [R][R]
+  double* LiT = Li + R * R;                                                 // [R][R]
+  float* ps = reinterpret_cast<float*>(LiT + R * R);                        // [B_ROWS][R]
+  double* dscr = reinterpret_cast<double*>(ps + B_ROWS * R);                // gram slice partials
+  __syncthreads();
+  for (int x = threadIdx.x; x < R * R; x += NT) Li[x] = __ldcg(p.Li_g + x);
+  for (int c0 = r0; c0 < r1; c0 += B_ROWS) {
+    const int nr = min(B_ROWS, r1 - c0);
+    apply_rinv<R>(p.P, p.P, c0, nr, Li, nullptr, false, p.fb_seed, ps, LiT);
+    if (gpart) {
+      for (int x = threadIdx.x; x < nr * R / 4; x += NT)
+        reinterpret_cast<float4*>(ps)[x] = __ldcg(reinterpret_cast<const float4*>(p.P + (size_t)c0 * R) + x);
+      __syncthreads();
+      gram_blocked<R>(ps, nr, gpart + (size_t)(c0 / B_ROWS) * npairs(R), dscr);
+      __syncthreads();
+    }
+  }
+}
+
+template <int R>
+__host__ __device__ constexpr size_t smem_fast_orth() {
+  // B: ps + gram slice partials; C: S, W, gd, red, flag; apply: Li, LiT, ps + slice partials
+  constexpr size_t nb4 = R / 4 < 1 ? 1 : R / 4;
+  constexpr size_t nblk = nb4 * (nb4 + 1) / 2;
+  constexpr size_t rs = (NT / nblk) < 1 ? 1 : (NT / nblk);
+  constexpr size_t dscr = rs > 1 ? (rs - 1) * nblk * 16 * 8 : 0;
+  constexpr size_t b = (size_t)B_ROWS * R * 4 + dscr;
+  constexpr size_t c = (2 * (size_t)R * R + R + 2 * NW) * 8 + 16;
+  constexpr size_t a = 2 * (size_t)R * R * 8 + b;
+  return a > c ? a : c;
+}
+
 // ------------------------------------------------------------------ phase D
 // Q_part[s][j][k] = sum_{i in split s} A[i][j] P_hat[i][k]
 template <int R>
@@ -779,16 +1059,27 @@ __device__ void phase_D(const Params& p, float* sm) {
 // ------------------------------------------------------------------ phase E
 template <int R>
 __device__ void phase_E(const Params& p) {
-  constexpr int UC = 32;   // columns per unit
-  const int units = (p.m + UC - 1) / UC;
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
-    const int c0 = u * UC, nc = min(UC, p.m - c0);
-    for (int x = threadIdx.x; x < nc * R; x += NT) {
-      const float* src = p.Q_part + (size_t)c0 * R + x;
-      float v = 0.f;
-      for (int s = 0; s < p.s2; s++) v += __ldcg(src + (size_t)s * p.m * R);
-      p.Qloc[(size_t)c0 * R + x] = v;
+  // Q = sum of the s2 partials, fixed order; 16-byte vectors over the whole
+  // m x R range (every CTA), 4 partials per step in flight
+  const size_t nv = (size_t)p.m * R / 4, stride = (size_t)p.m * R / 4;
+  const float4* src = reinterpret_cast<const float4*>(p.Q_part);
+  float4* dst = reinterpret_cast<float4*>(p.Qloc);
+  for (size_t x = (size_t)blockIdx.x * NT + threadIdx.x; x < nv; x += (size_t)gridDim.x * NT) {
+    float4 v = __ldcg(src + x);
+    int s = 1;
+    for (; s + 3 < p.s2; s += 4) {
+      const float4 a = __ldcg(src + x + (size_t)s * stride), b = __ldcg(src + x + (size_t)(s + 1) * stride);
+      const float4 c = __ldcg(src + x + (size_t)(s + 2) * stride), d = __ldcg(src + x + (size_t)(s + 3) * stride);
+      v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+      v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
+      v.x += c.x; v.y += c.y; v.z += c.z; v.w += c.w;
+      v.x += d.x; v.y += d.y; v.z += d.z; v.w += d.w;
     }
+    for (; s < p.s2; s++) {
+      const float4 a = __ldcg(src + x + (size_t)s * stride);
+      v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+    }
+    dst[x] = v;
   }
 }
 

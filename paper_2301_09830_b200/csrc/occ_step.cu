@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 namespace occ {
 
@@ -22,6 +23,40 @@ __global__ void __launch_bounds__(NT, 1) occ_step_kernel(const __grid_constant__
   auto bar = [&]() { nb++; grid_barrier(p.bar, nb * gridDim.x); };
   const bool stamp = coop && blockIdx.x == 0 && threadIdx.x == 0;
   if (stamp) p.stats->t_ns[0] = gtimer();
+  // a4 with the one-CTA factorisation (occ_kernels.cuh, fast orthonormalisation);
+  // a degenerate column takes phases C1 / C2 / C3
+  auto orth_fast = [&](bool do_reduce) {
+    const int units = (p.n + B_ROWS - 1) / B_ROWS;
+    phase_B_fast<R>(p, p.P, p.G_part, do_reduce, smraw);
+    bar();
+    OCC_STAMP(p, 9);
+    if (blockIdx.x == 0) {
+      const int plan = factor_fast<R>(p, p.G_part, true, true, smraw);
+      if (threadIdx.x == 0) p.ctl[1] = plan;
+    }
+    bar();
+    OCC_STAMP(p, 10);
+    const int plan = __ldcg(p.ctl + 1);
+    if (plan == 2) {
+      OrthSmem<R>& o = *reinterpret_cast<OrthSmem<R>*>(smraw);
+      float* ps = reinterpret_cast<float*>(smraw + orth_bytes<R>());
+      int pl = phase_C1<R>(p, o, ps);
+      if (pl == 2) { bar(); pl = phase_C2<R>(p, o, ps); }
+      if (pl == 3) { bar(); phase_C3<R>(p, o, ps); }
+      return;
+    }
+    if (plan == 3) {   // CholQR2: P_hat of the first pass and its Gram, a second factorisation
+      for (int u = blockIdx.x; u < units; u += gridDim.x)
+        apply_fast<R>(p, u * B_ROWS, min(p.n, (u + 1) * B_ROWS), smraw, p.G2_part);
+      bar();
+      if (blockIdx.x == 0) factor_fast<R>(p, p.G2_part, false, false, smraw);
+      bar();
+    }
+    const int r0 = (int)((long long)blockIdx.x * p.n / gridDim.x);
+    const int r1 = (int)((long long)(blockIdx.x + 1) * p.n / gridDim.x);
+    apply_fast<R>(p, r0, r1, smraw, nullptr);
+    OCC_STAMP(p, 11);
+  };
   for (int ph = ph0; ph < ph1; ph++) {
     switch (ph) {
       case P_A:   // tensor-core sweep 1 (occ_tc.cuh)
@@ -29,12 +64,28 @@ __global__ void __launch_bounds__(NT, 1) occ_step_kernel(const __grid_constant__
         else tc::phase_A_tc<R, false>(p, smraw);
         break;
       case P_B1: {
+        if (coop && p.fast_orth && ph1 > P_C3) {   // P reduce + Gram + orthonormalisation (orth_fast)
+          orth_fast(true);
+          ph = P_C3;
+          break;
+        }
+        if (p.fast_orth && ph1 <= P_B2) {           // the P reduce alone, over every CTA
+          reduce_p_all<R>(p);
+          break;
+        }
         const bool g = ph1 > P_B2;
         phase_B<R>(p, sm, true, g);
         if (g) ph = P_B2;
         break;
       }
-      case P_B2: phase_B<R>(p, sm, false, true); break;
+      case P_B2:
+        if (coop && p.fast_orth && ph1 > P_C3) {
+          orth_fast(false);
+          ph = P_C3;
+          break;
+        }
+        phase_B<R>(p, sm, false, true);
+        break;
       case P_C1: {
         OrthSmem<R>& o = *reinterpret_cast<OrthSmem<R>*>(smraw);
         float* ps = reinterpret_cast<float*>(smraw + orth_bytes<R>());
@@ -105,7 +156,7 @@ static size_t smem_bytes_for(const Geometry& g) {
   size_t d = tc::smem_D_tc<R>(g.rs2);
   size_t f = std::max(2 * (size_t)F_ROWS * R * 4,   // P rows + Ploc rows (DP, OCC_ORIENT_T)
                       tc::smem_F_tc<R>());
-  return std::max({a, b, c, d, f});
+  return std::max({a, b, c, d, f, smem_fast_orth<R>()});
 }
 
 static int num_sms() {
@@ -179,7 +230,8 @@ WsLayout make_layout(const Geometry& g, int nmat) {
   L.p_bucket = off; off = al(off + (size_t)nmat * g.n * R * 4);
   L.qw_bucket = off; off = al(off + (size_t)nmat * g.m * R * 4);
   L.qs_bucket = off; off = al(off + (size_t)nmat * std::max(g.n, g.m) * R * 4);   // reduced Q (or V, OCC_ORIENT_T)
-  L.qt = off; off = al(off + umma_qt_bytes(g.n, g.m, R));   // tcgen05 sweeps: Q^T / P_hat^T split hi / lo
+  L.qt = off; off = al(off + umma_qt_bytes(g.n, g.m, R));
+  L.li = off; off = al(off + (size_t)R * R * 8);               // Li of the one-CTA factorisation   // tcgen05 sweeps: Q^T / P_hat^T split hi / lo
   L.v2_tail_bytes = v2_tail_bytes(g.n, g.m, R, 148);   // reused by every matrix of a multi-matrix call
   L.v2_tail = off; off = al(off + L.v2_tail_bytes);
   L.total = off;
@@ -197,6 +249,12 @@ void fill_ws(Params& p, const Geometry& g, const WsLayout& L, void* ws) {
   p.G2_part = reinterpret_cast<double*>(base + L.g2_part);
   p.XY_part = reinterpret_cast<double*>(base + L.xy_part);
   p.Qt = reinterpret_cast<float*>(base + L.qt);
+  p.Li_g = reinterpret_cast<double*>(base + L.li);
+  static const bool fast = [] {
+    const char* e = getenv("OCC_FAST_ORTH");
+    return !(e && e[0] == '0');
+  }();
+  p.fast_orth = fast ? 1 : 0;
   p.s1 = g.s1; p.cs1 = g.cs1; p.s2 = g.s2; p.rs2 = g.rs2; p.ngp = g.ngp;
 }
 
@@ -204,9 +262,9 @@ void fill_ws(Params& p, const Geometry& g, const WsLayout& L, void* ws) {
 // launch (grid = co-resident CTAs); otherwise one launch per phase group.
 template <int R, bool DPL>
 static cudaError_t run_t(Params p, const Geometry& g, int ph0, int ph1, bool multi, cudaStream_t st) {
-  if (ph0 == P_A && ph1 > P_A) {   // sweep 1 on the tcgen05 path (occ_umma.cu) when it applies
+  if (ph0 == P_A && ph1 > P_A && umma_applies(p, R)) {   // sweep 1 on the tcgen05 path (occ_umma.cu)
     int G = 0;
-    const cudaError_t eu = run_umma_sweep1(p, R, g.s1, &G, st);
+    const cudaError_t eu = run_umma_sweep(p, R, false, g.s1, &G, st);
     if (eu == cudaSuccess) {
       p.s1 = G;
       ph0 = P_B1;
@@ -214,6 +272,26 @@ static cudaError_t run_t(Params p, const Geometry& g, int ph0, int ph1, bool mul
     } else if (eu != cudaErrorNotSupported) {
       return eu;
     }
+  }
+  if (ph0 <= P_D && P_D < ph1 && umma_applies(p, R)) {   // sweep 2 on the tcgen05 path
+    if (ph0 < P_D) {
+      const cudaError_t e0 = run_t<R, DPL>(p, g, ph0, P_D, multi, st);
+      if (e0 != cudaSuccess) return e0;
+      ph0 = P_D;
+    }
+    int G = 0;
+    const cudaError_t eu = run_umma_sweep(p, R, true, g.s2, &G, st);
+    if (eu == cudaSuccess) {
+      p.s2 = G;
+      ph0 = P_E;
+      if (ph0 >= ph1) return cudaSuccess;
+    } else if (eu != cudaErrorNotSupported) {
+      return eu;
+    }
+  }
+  if (ph0 == P_F && ph1 == P_END && p.f_tc && umma_applies(p, R)) {   // the DP reconstruction on tcgen05
+    const cudaError_t eu = run_umma_recon(p, R, st);
+    if (eu != cudaErrorNotSupported) return eu;
   }
   auto kern = occ_step_kernel<R, DPL>;
   const size_t smem = smem_bytes_for<R>(g);
