@@ -21,7 +21,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libocc.so")
 LIB_TRACE = os.path.join(HERE, "libocc_trace.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("occ_api.cu", "occ_step.cu", "occ_v2.cu", "occ_umma.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("occ_api.cu", "occ_step.cu", "occ_v2.cu", "occ_umma.cu")] + \
+    [os.path.join(HERE, "csrc", f"occ_step_r{r}.cu") for r in (4, 8, 16, 32, 64)]
 DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + \
     glob.glob(os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "occ.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

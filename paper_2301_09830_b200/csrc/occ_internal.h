@@ -24,7 +24,7 @@ constexpr size_t kBarLinesBytes = 8 * 128;                        // (v2::kBarLi
 
 struct WsLayout {
   size_t bar = 0, p_part = 0, q_part = 0, g_part = 0, g2_part = 0, xy_part = 0;
-  size_t p_bucket = 0, qw_bucket = 0, qs_bucket = 0, qt = 0, li = 0, v2_tail = 0, v2_tail_bytes = 0, total = 0;
+  size_t p_bucket = 0, qw_bucket = 0, qs_bucket = 0, qt = 0, li = 0, gred = 0, v2_tail = 0, v2_tail_bytes = 0, total = 0;
 };
 
 Geometry make_geometry(int64_t n, int64_t m, int r, int sms);
@@ -34,6 +34,17 @@ void fill_ws(Params& p, const Geometry& g, const WsLayout& L, void* ws);
 cudaError_t run_phases(const Params& p, const Geometry& g, int ph0, int ph1, bool multi, bool dpl,
                        cudaStream_t st);
 cudaError_t run_decompress(const Params& p, int r, cudaStream_t st);
+// one rank's step kernels (occ_step_r{4..64}.cu)
+#define OCC_DECL_STEP(RR)                                                                               \
+  cudaError_t run_phases_r##RR(const Params& p, const Geometry& g, int ph0, int ph1, bool multi, bool dpl, \
+                               cudaStream_t st);                                                        \
+  unsigned take_nonfinite_v1_r##RR();
+OCC_DECL_STEP(4)
+OCC_DECL_STEP(8)
+OCC_DECL_STEP(16)
+OCC_DECL_STEP(32)
+OCC_DECL_STEP(64)
+#undef OCC_DECL_STEP
 size_t v2_tail_bytes(int64_t n, int64_t m, int r, int sms);
 cudaError_t run_v2(const Params& p, int r, void* ws_tail, size_t tail_avail, int sms, cudaStream_t st);
 // OCC_CHECK_FINITE: read and clear the device status words (occ_check_status)

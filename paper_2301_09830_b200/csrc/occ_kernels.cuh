@@ -145,6 +145,7 @@ struct Params {
   LinkPush push;         // occ_link sender: the fused kernel pushes the factors itself
   float* Qt;             // workspace: the small factor transposed and split hi / lo (occ_umma.cu)
   double* Li_g;          // workspace: D^-1/2 L^-1 of the one-CTA factorisation (fast orthonormalisation)
+  double* G_red;         // workspace: the reduced Gram (packed upper triangle) of the fast orthonormalisation
   int fast_orth;         // per-phase path: one-CTA factorisation between two grid barriers (orth_fast)
 };
 
@@ -770,15 +771,14 @@ __device__ void reduce_p_all(const Params& p) {
   }
 }
 
-// Packed upper-triangle Gram of ps[0 .. nr) (fp32 rows) in fp64: 4 x 4 blocks
-// (a0 .. a0+3, b0 .. b0+3), a0 <= b0, each thread one block over a row slice;
-// slices combined through shared memory in a fixed order.
+// Packed upper-triangle Gram of pd[0 .. nr) (rows already converted to fp64)
+// in fp64: 4 x 4 blocks (a0 .. a0+3, b0 .. b0+3), a0 <= b0, each thread one
+// block over a row slice; slices combined through shared memory in a fixed order.
 template <int R>
-__device__ void gram_blocked(const float* ps, int nr, double* out, double* dscr) {
+__device__ void gram_blocked(const double* pd, int nr, double* out, double* dscr) {
   constexpr int NB4 = R / 4 < 1 ? 1 : R / 4;
   constexpr int NBLK = NB4 * (NB4 + 1) / 2;
   constexpr int RS = (NT / NBLK) < 1 ? 1 : (NT / NBLK);     // row slices
-  constexpr int NP = npairs(R);
   const int t = threadIdx.x;
   double g[4][4];
 #pragma unroll
@@ -789,14 +789,16 @@ __device__ void gram_blocked(const float* ps, int nr, double* out, double* dscr)
   int A = 0, rem = blk;
   while (rem >= NB4 - A) { rem -= NB4 - A; A++; }
   const int B = A + rem;
-  const bool act = sl < RS && R >= 4;
+  const bool act = sl < RS;
   if (act) {
     const int i0 = (int)((long long)sl * nr / RS), i1 = (int)((long long)(sl + 1) * nr / RS);
     for (int i = i0; i < i1; i++) {
-      const float4 xa = *reinterpret_cast<const float4*>(ps + i * R + 4 * A);
-      const float4 xb = *reinterpret_cast<const float4*>(ps + i * R + 4 * B);
-      const double a4[4] = {(double)xa.x, (double)xa.y, (double)xa.z, (double)xa.w};
-      const double b4[4] = {(double)xb.x, (double)xb.y, (double)xb.z, (double)xb.w};
+      const double2 a01 = *reinterpret_cast<const double2*>(pd + i * R + 4 * A);
+      const double2 a23 = *reinterpret_cast<const double2*>(pd + i * R + 4 * A + 2);
+      const double2 b01 = *reinterpret_cast<const double2*>(pd + i * R + 4 * B);
+      const double2 b23 = *reinterpret_cast<const double2*>(pd + i * R + 4 * B + 2);
+      const double a4[4] = {a01.x, a01.y, a23.x, a23.y};
+      const double b4[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
       for (int u = 0; u < 4; u++)
 #pragma unroll
@@ -829,48 +831,70 @@ __device__ void gram_blocked(const float* ps, int nr, double* out, double* dscr)
         if (a <= b) out[pidx(R, a, b)] = g[u][v];
       }
   }
-  if (R < 4 && t < NP) {   // (R < 4 is not instantiated; kept total)
-    int a = 0, rr = t;
-    while (rr >= R - a) { rr -= R - a; a++; }
-    const int b = a + rr;
-    double v = 0.0;
-    for (int i = 0; i < nr; i++) v = fma((double)ps[i * R + a], (double)ps[i * R + b], v);
-    out[t] = v;
-  }
 }
 
-// phase B of the fast orthonormalisation: per 128-row unit, P reduce (or P read)
-// and the fp64 Gram partial into part[u].
+// phase B of the fast orthonormalisation: per 128-row unit of src (P, already
+// reduced), the fp64 Gram partial into part[u].
 template <int R>
-__device__ void phase_B_fast(const Params& p, const float* src, double* part, bool do_reduce, unsigned char* smraw) {
+__device__ void phase_B_fast(const Params& p, const float* src, double* part, unsigned char* smraw) {
   const int units = (p.n + B_ROWS - 1) / B_ROWS;
-  float* ps = reinterpret_cast<float*>(smraw);                                // [B_ROWS][R]
-  double* dscr = reinterpret_cast<double*>(smraw + (size_t)B_ROWS * R * 4);   // slice partials
+  double* pd = reinterpret_cast<double*>(smraw);                            // [B_ROWS][R]
+  double* dscr = pd + (size_t)B_ROWS * R;                                   // slice partials
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int r0 = u * B_ROWS, nr = min(B_ROWS, p.n - r0);
     __syncthreads();
-    if (do_reduce) {
-      reduce_p_rows<R>(p, r0, nr, ps);
-    } else {
-      for (int x = threadIdx.x; x < nr * R / 4; x += NT)
-        reinterpret_cast<float4*>(ps)[x] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)r0 * R) + x);
+    for (int x = threadIdx.x; x < nr * R / 4; x += NT) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(src + (size_t)r0 * R) + x);
+      reinterpret_cast<double2*>(pd)[2 * x] = make_double2(v.x, v.y);
+      reinterpret_cast<double2*>(pd)[2 * x + 1] = make_double2(v.z, v.w);
     }
     __syncthreads();
-    gram_blocked<R>(ps, nr, part + (size_t)u * npairs(R), dscr);
+    gram_blocked<R>(pd, nr, part + (size_t)u * npairs(R), dscr);
+  }
+}
+
+// The Gram partials reduced over every CTA: 8 threads per packed entry, each
+// summing every 8th partial, then a fixed 8-lane shuffle tree (deterministic).
+template <int R>
+__device__ void reduce_gram_all(const double* __restrict__ part, int npart, double* out) {
+  constexpr int NP = npairs(R);
+  const int lane8 = threadIdx.x & 7;
+  for (int base = (blockIdx.x * NT + threadIdx.x) >> 3; base < ((NP + 3) / 4) * 4; base += (gridDim.x * NT) >> 3) {
+    const int q = base;
+    double g = 0.0;
+    if (q < NP) {
+      double g0 = 0.0, g1 = 0.0;
+      int u = lane8;
+      for (; u + 8 < npart; u += 16) {
+        g0 += __ldcg(part + (size_t)u * NP + q);
+        g1 += __ldcg(part + (size_t)(u + 8) * NP + q);
+      }
+      if (u < npart) g0 += __ldcg(part + (size_t)u * NP + q);
+      g = g0 + g1;
+    }
+    g += __shfl_xor_sync(0xffffffffu, g, 1);
+    g += __shfl_xor_sync(0xffffffffu, g, 2);
+    g += __shfl_xor_sync(0xffffffffu, g, 4);
+    if (lane8 == 0 && q < NP) out[q] = g;
   }
 }
 
 // CTA 0: Gram reduce + LDL^T with the inverse carried along.  Writes Li =
-// D^-1/2 L^-1 (R x R, lower, row-major) to p.Li_g and returns the plan:
-// 2 a degenerate column (detect), 3 the CholQR2 pass is needed, 0 done.
+// D^-1/2 L^-1 TRANSPOSED (p.Li_g[k R + i] = Li[i][k], the layout apply_fast
+// reads) and returns the plan: 2 a degenerate column (detect), 3 the CholQR2
+// pass is needed, 0 done.  S and W are stored column-major and thread x of a
+// step owns row i = j + 1 + x % R (consecutive threads, consecutive rows:
+// conflict-free; the pivot-column operands are broadcasts).
 template <int R>
-__device__ int factor_fast(const Params& p, const double* part, bool detect, bool first_pass, unsigned char* smraw) {
-  double* S = reinterpret_cast<double*>(smraw);   // [R][R] Gram -> eliminated
-  double* W = S + R * R;                           // [R][R] unit-lower inverse
+__device__ int factor_fast(const Params& p, const double* part, int npart, bool detect, bool first_pass,
+                           unsigned char* smraw) {
+  double* S = reinterpret_cast<double*>(smraw);   // column-major: S[k R + i] = S(i, k)
+  double* W = S + R * R;                           // column-major unit-lower inverse
   double* gd = W + R * R;                          // [R] Gram diagonal
   double* red = gd + R;                            // [2][NW] norms
   int* flag = reinterpret_cast<int*>(red + 2 * NW);
   constexpr int NP = npairs(R);
+  constexpr int TK = (NT / R) < R ? (NT / R) : R;  // threads along k per row
   const double tau2 = p.tau * p.tau;
   for (int q = threadIdx.x; q < NP; q += NT) {
     int a = 0, rem = q;
@@ -878,13 +902,13 @@ __device__ int factor_fast(const Params& p, const double* part, bool detect, boo
     const int b = a + rem;
     double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;   // fixed order per entry
     int u = 0;
-    for (; u + 3 < p.ngp; u += 4) {
+    for (; u + 3 < npart; u += 4) {
       g0 += __ldcg(part + (size_t)u * NP + q);
       g1 += __ldcg(part + (size_t)(u + 1) * NP + q);
       g2 += __ldcg(part + (size_t)(u + 2) * NP + q);
       g3 += __ldcg(part + (size_t)(u + 3) * NP + q);
     }
-    for (; u < p.ngp; u++) g0 += __ldcg(part + (size_t)u * NP + q);
+    for (; u < npart; u++) g0 += __ldcg(part + (size_t)u * NP + q);
     const double g = (g0 + g1) + (g2 + g3);
     S[a * R + b] = g;
     S[b * R + a] = g;
@@ -896,36 +920,60 @@ __device__ int factor_fast(const Params& p, const double* part, bool detect, boo
   if (first_pass && p.check_finite && threadIdx.x < R && !isfinite(S[threadIdx.x * R + threadIdx.x]))
     atomicOr(&g_nonfinite_v1, 1u);
   __syncthreads();
+  OCC_STAMP(p, 2);
+  const int ti = threadIdx.x % R, tk = threadIdx.x / R;
   for (int j = 0; j < R; j++) {
     const double d = S[j * R + j], gj = gd[j];
     if (detect && (gj == 0.0 || !(d >= tau2 * gj))) return 2;   // uniform
-    const double rinv = 1.0 / (d > 0.0 ? d : 1e-300);
-    // rows i > j: S[i][k] -= l_ij S[k][j] (j < k <= i), W[i][k] -= l_ij W[j][k] (k <= j)
-    const int rows = R - 1 - j;
-    for (int x = threadIdx.x; x < rows * R; x += NT) {
-      const int i = j + 1 + x / R, k = x % R;
-      if (k > i) continue;
-      const double l = S[i * R + j] * rinv;
-      if (k > j) S[i * R + k] = fma(-l, S[k * R + j], S[i * R + k]);
-      else W[i * R + k] = fma(-l, W[j * R + k], W[i * R + k]);
+    const double rinv = __drcp_rn(d > 0.0 ? d : 1e-300);       // = 1.0 / d (both correctly rounded)
+    // rows i > j: S(i,k) -= l_ij S(k,j) (j < k <= i); W(i,k) -= l_ij W(j,k) (k <= j)
+    const int i = j + 1 + ti;
+    if (tk < TK && i < R) {
+      // every operand of the step loaded before any store (the stores cannot
+      // alias the loads of another k, but the compiler cannot know)
+      constexpr int KU = R / TK;
+      const double l = S[j * R + i] * rinv;
+      double tv[KU], pv[KU];
+      // S(i,k) for k > j, W(i,k) for k <= j: one address select, no branch
+      // around the loads (a divergent branch per element serialised them)
+#pragma unroll
+      for (int u = 0; u < KU; u++) {
+        const int k = tk + u * TK;
+        const bool lo = k <= j;
+        const double* t = (lo ? W : S) + k * R + i;
+        const double* pp = lo ? (W + k * R + j) : (S + j * R + k);
+        tv[u] = *t;
+        pv[u] = *pp;
+      }
+#pragma unroll
+      for (int u = 0; u < KU; u++) {
+        const int k = tk + u * TK;
+        double* t = ((k <= j) ? W : S) + k * R + i;
+        if (k <= i) *t = fma(-l, pv[u], tv[u]);
+      }
     }
     __syncthreads();
   }
+  OCC_STAMP(p, 3);
   // Li = D^-1/2 W; kappa_est = ||L D^1/2||_F ||D^-1/2 L^-1||_F
+  double* sd = red + 2 * NW + 2;                   // [R] d_i^-1/2, then [R] 1 / d_i
+  for (int x = threadIdx.x; x < R; x += NT) {
+    const double di = S[x * R + x];
+    sd[x] = 1.0 / sqrt(di > 0.0 ? di : 1e-300);
+    sd[R + x] = __drcp_rn(di > 0.0 ? di : 1e-300);
+  }
+  __syncthreads();
   double nl = 0.0, ni = 0.0;
   for (int x = threadIdx.x; x < R * R; x += NT) {
-    const int i = x / R, k = x % R;
-    const double di = S[i * R + i];
-    const double si = 1.0 / sqrt(di > 0.0 ? di : 1e-300);
-    const double li = (k <= i) ? W[x] * si : 0.0;
-    p.Li_g[x] = li;
+    const int i = x % R, k = x / R;                // x = k R + i
+    const double li = (k <= i) ? W[x] * sd[i] : 0.0;
+    p.Li_g[x] = li;                                // transposed: [k][i]
     ni = fma(li, li, ni);
     if (k < i) {
-      const double dk = S[k * R + k];
-      const double lk = S[x] / (dk > 0.0 ? dk : 1e-300);
-      nl = fma(lk * lk, dk, nl);
+      const double lk = S[x] * sd[R + k];
+      nl = fma(lk * lk, S[k * R + k], nl);
     } else if (k == i) {
-      nl += di;
+      nl += S[x];
     }
   }
 #pragma unroll
@@ -938,8 +986,8 @@ __device__ int factor_fast(const Params& p, const double* part, bool detect, boo
     red[NW + (threadIdx.x >> 5)] = ni;
   }
   __syncthreads();
-  int plan = 0;
   if (threadIdx.x == 0) {
+    int plan = 0;
     double a = 0.0, b = 0.0;
     for (int w = 0; w < NW; w++) { a += red[w]; b += red[NW + w]; }
     const double kappa = sqrt(a) * sqrt(b);
@@ -952,43 +1000,74 @@ __device__ int factor_fast(const Params& p, const double* part, bool detect, boo
     *flag = plan;
   }
   __syncthreads();
+  OCC_STAMP(p, 4);
   return *flag;
 }
 
-// every CTA: P_hat = P Li^T on rows [r0, r1) (Li from p.Li_g), chunks of
-// B_ROWS; with gpart (the CholQR2 first pass; r0 on a unit boundary) also the
-// Gram partial of each unit of P_hat.
+// every CTA: P_hat = P Li^T on rows [r0, r1) (LiT = Li^T from p.Li_g), chunks
+// of B_ROWS, fp64 sums as apply_rinv; with gpart (the CholQR2 first pass; r0 on
+// a unit boundary) also the Gram partial of each unit of P_hat.
 template <int R>
 __device__ void apply_fast(const Params& p, int r0, int r1, unsigned char* smraw, double* gpart) {
-  double* Li = reinterpret_cast<double*>(smraw);                            // [R][R]
-  double* LiT = Li + R * R;                                                 // [R][R]
+  constexpr int KPT = (R >= 16) ? 8 : R;   // outputs per thread; R / KPT threads per row
+  constexpr int TPR = R / KPT;
+  double* LiT = reinterpret_cast<double*>(smraw);                           // [R][R]: LiT[b][a] = Li[a][b]
   float* ps = reinterpret_cast<float*>(LiT + R * R);                        // [B_ROWS][R]
-  double* dscr = reinterpret_cast<double*>(ps + B_ROWS * R);                // gram slice partials
+  double* pd = reinterpret_cast<double*>(ps + B_ROWS * R);                  // [B_ROWS][R] (gram)
+  double* dscr = pd + (size_t)B_ROWS * R;                                   // gram slice partials
   __syncthreads();
-  for (int x = threadIdx.x; x < R * R; x += NT) Li[x] = __ldcg(p.Li_g + x);
+  for (int x = threadIdx.x; x < R * R / 2; x += NT)
+    reinterpret_cast<double2*>(LiT)[x] = __ldcg(reinterpret_cast<const double2*>(p.Li_g) + x);
   for (int c0 = r0; c0 < r1; c0 += B_ROWS) {
     const int nr = min(B_ROWS, r1 - c0);
-    apply_rinv<R>(p.P, p.P, c0, nr, Li, nullptr, false, p.fb_seed, ps, LiT);
+    __syncthreads();
+    for (int x = threadIdx.x; x < nr * R; x += NT) ps[x] = __ldcg(p.P + (size_t)c0 * R + x);
+    __syncthreads();
+    for (int x = threadIdx.x; x < nr * TPR; x += NT) {
+      const int i = x / TPR, a0 = (x % TPR) * KPT;
+      double acc[KPT];
+#pragma unroll
+      for (int j = 0; j < KPT; j++) acc[j] = 0.0;
+      const int bmax = min(R, a0 + KPT);   // Li is lower: LiT[b][a] = 0 for b > a
+#pragma unroll 4
+      for (int b = 0; b < bmax; b++) {
+        const double pb = (double)ps[i * R + b];
+        const double2* lt = reinterpret_cast<const double2*>(LiT + b * R + a0);
+#pragma unroll
+        for (int j = 0; j < KPT / 2; j++) {
+          const double2 l = lt[j];
+          acc[2 * j] = fma(pb, l.x, acc[2 * j]);
+          acc[2 * j + 1] = fma(pb, l.y, acc[2 * j + 1]);
+        }
+      }
+      float o[KPT];
+#pragma unroll
+      for (int j = 0; j < KPT; j++) o[j] = (float)acc[j];
+      float* dst = p.P + (size_t)(c0 + i) * R + a0;
+#pragma unroll
+      for (int j = 0; j < KPT; j++) dst[j] = o[j];
+      if (gpart) {
+#pragma unroll
+        for (int j = 0; j < KPT; j++) pd[i * R + a0 + j] = (double)o[j];
+      }
+    }
     if (gpart) {
-      for (int x = threadIdx.x; x < nr * R / 4; x += NT)
-        reinterpret_cast<float4*>(ps)[x] = __ldcg(reinterpret_cast<const float4*>(p.P + (size_t)c0 * R) + x);
       __syncthreads();
-      gram_blocked<R>(ps, nr, gpart + (size_t)(c0 / B_ROWS) * npairs(R), dscr);
-      __syncthreads();
+      gram_blocked<R>(pd, nr, gpart + (size_t)(c0 / B_ROWS) * npairs(R), dscr);
     }
   }
 }
 
 template <int R>
 __host__ __device__ constexpr size_t smem_fast_orth() {
-  // B: ps + gram slice partials; C: S, W, gd, red, flag; apply: Li, LiT, ps + slice partials
+  // B: pd + gram slice partials; C: S, W, gd, red, flag; apply: LiT, ps, pd + slice partials
   constexpr size_t nb4 = R / 4 < 1 ? 1 : R / 4;
   constexpr size_t nblk = nb4 * (nb4 + 1) / 2;
   constexpr size_t rs = (NT / nblk) < 1 ? 1 : (NT / nblk);
   constexpr size_t dscr = rs > 1 ? (rs - 1) * nblk * 16 * 8 : 0;
-  constexpr size_t b = (size_t)B_ROWS * R * 4 + dscr;
-  constexpr size_t c = (2 * (size_t)R * R + R + 2 * NW) * 8 + 16;
-  constexpr size_t a = 2 * (size_t)R * R * 8 + b;
+  constexpr size_t b = (size_t)B_ROWS * R * 8 + dscr;
+  constexpr size_t c = (2 * (size_t)R * R + 3 * R + 2 * NW + 2) * 8 + 16;
+  constexpr size_t a = (size_t)R * R * 8 + (size_t)B_ROWS * R * 4 + b;
   return a > c ? a : c;
 }
 

@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 namespace occ {
 namespace umma {
@@ -360,13 +361,18 @@ constexpr int BC = 128;     // columns per band (MMA M)
 constexpr int TR = 64;      // rows per tile (MMA N)
 constexpr int NTH = 320;    // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 constexpr int NEP = 256;    // epilogue threads
-constexpr int NS = 2;       // row-factor stages
+constexpr int NSMAX = 3;    // row-factor stages (as many as shared memory holds, at most 3)
 template <int R>
 struct Cfg {
   static constexpr int CBOX = BC * R * 4;       // one column-factor operand (hi or lo), all K blocks
   static constexpr int RBOX = TR * R * 4;       // one row-factor operand
+  static constexpr int stages(bool two_c, bool two_r) {
+    const int left = kSmemCap - (two_c ? 4 : 2) * CBOX - 1024 - 512;
+    const int ns = left / ((two_r ? 4 : 2) * RBOX);
+    return ns < NSMAX ? ns : NSMAX;
+  }
   static constexpr int smem(bool two_c, bool two_r) {
-    return (two_c ? 4 : 2) * CBOX + NS * (two_r ? 4 : 2) * RBOX + 1024 + 512;
+    return (two_c ? 4 : 2) * CBOX + stages(two_c, two_r) * (two_r ? 4 : 2) * RBOX + 1024 + 512;
   }
 };
 }  // namespace rc
@@ -376,6 +382,8 @@ struct RcArgs {
   int two_c, two_r;             // the e_new product has its own column / row factor
   int dpl;                      // e_new = A - D2 (else A - round(D1))
   int has_e, r_bf16;
+  int terms;                    // 3 (the fp32-level split); 1 only as a timing experiment (OCC_RC_TERMS)
+  int ns;                       // row-factor stages
   const float* M; long long ldm;
   const float* E; long long lde;
   void* out; long long ldo;     // M' (nullptr: not written)
@@ -398,12 +406,13 @@ __global__ void __launch_bounds__(rc::NTH, 1)
   const int ncop = a.two_c ? 4 : 2, nrop = a.two_r ? 4 : 2;
   unsigned char* cbase = sm;                                   // [ncop][KB][128 rows][128 B]
   unsigned char* rbase = sm + ncop * C::CBOX;                  // [NS][nrop][KB][64 rows][128 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rbase + rc::NS * nrop * C::RBOX);
+  const int NS = a.ns;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rbase + NS * nrop * C::RBOX);
   uint64_t* cfull = bars;
   uint64_t* cempty = bars + 1;
   uint64_t* rfull = bars + 2;                 // [NS]
-  uint64_t* rempty = rfull + rc::NS;          // [NS]
-  uint64_t* accf = rempty + rc::NS;           // [2]
+  uint64_t* rempty = rfull + NS;              // [NS]
+  uint64_t* accf = rempty + NS;               // [2]
   uint64_t* acce = accf + 2;                  // [2]
   unsigned* tmem_hold = reinterpret_cast<unsigned*>(acce + 2);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -418,7 +427,7 @@ __global__ void __launch_bounds__(rc::NTH, 1)
   if (tid == 0) {
     mbar_init(cfull, 1);
     mbar_init(cempty, 1);
-    for (int s = 0; s < rc::NS; s++) {
+    for (int s = 0; s < NS; s++) {
       mbar_init(&rfull[s], 1);
       mbar_init(&rempty[s], 1);
     }
@@ -440,16 +449,33 @@ __global__ void __launch_bounds__(rc::NTH, 1)
     t_hi = (int)((long long)(gi + 1) * a.ntile / a.G);
   };
 
-  if (w == 0) {
-    if (lane == 0) {   // ------------------------------------------------ TMA producer
-      const unsigned long long pol = v2::l2_evict_normal();
-      int s = 0;
-      unsigned ph = 0, cph = 0;
-      for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        int band, t_lo, t_hi;
-        range(it, band, t_lo, t_hi);
+  if (w == 0) {   // ------------------------------------------------ TMA producer (lane 0) + L2 prefetch (warp)
+    const unsigned long long pol = v2::l2_evict_normal();
+    int s = 0;
+    unsigned ph = 0, cph = 0;
+    // the tile's rows of M and e (this band's 128 columns: 512 B each) into L2,
+    // PF tiles ahead of the epilogue, whose per-lane column loads then hit L2
+    constexpr int PF = 3;
+    auto prefetch_tile = [&](int band, int t) {
+      const int c0 = band * rc::BC;
+      const unsigned bytes = (unsigned)min(rc::BC, a.m - c0) * 4u;
+#pragma unroll
+      for (int h = 0; h < rc::TR / 32; h++) {
+        const int i = t * rc::TR + 32 * h + lane;
+        if (i < a.n) {
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.M + (size_t)i * a.ldm + c0), "r"(bytes)
+                       : "memory");
+          if (a.has_e)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.E + (size_t)i * a.lde + c0), "r"(bytes)
+                         : "memory");
+        }
+      }
+    };
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+      int band, t_lo, t_hi;
+      range(it, band, t_lo, t_hi);
+      if (lane == 0) {
         mbar_wait(cempty, cph ^ 1u);
-        cph ^= 1u;
         mbar_expect_tx(cfull, ncop * C::CBOX);
 #pragma unroll
         for (int kb = 0; kb < KB; kb++) {
@@ -460,7 +486,12 @@ __global__ void __launch_bounds__(rc::NTH, 1)
             tma_2d(cop(3) + kb * CB1, &tC2l, 32 * kb, band * rc::BC, cfull, pol);
           }
         }
-        for (int t = t_lo; t < t_hi; t++) {
+      }
+      cph ^= 1u;
+      __syncwarp();
+      for (int t = t_lo; t < min(t_hi, t_lo + PF); t++) prefetch_tile(band, t);
+      for (int t = t_lo; t < t_hi; t++) {
+        if (lane == 0) {
           mbar_wait(&rempty[s], ph ^ 1u);
           mbar_expect_tx(&rfull[s], nrop * C::RBOX);
 #pragma unroll
@@ -472,8 +503,10 @@ __global__ void __launch_bounds__(rc::NTH, 1)
               tma_2d(rop(s, 3) + kb * RB1, &tR2l, 32 * kb, t * rc::TR, &rfull[s], pol);
             }
           }
-          if (++s == rc::NS) { s = 0; ph ^= 1u; }
         }
+        __syncwarp();
+        if (t + PF < t_hi) prefetch_tile(band, t + PF);
+        if (++s == NS) { s = 0; ph ^= 1u; }
       }
     }
   } else if (w == 1) {
@@ -500,22 +533,26 @@ __global__ void __launch_bounds__(rc::NTH, 1)
             const uint64_t c1h = desc_k_sw128(smem_u32(cop(0)) + co), c1l = desc_k_sw128(smem_u32(cop(1)) + co);
             const uint64_t r1h = desc_k_sw128(smem_u32(rop(s, 0)) + ro), r1l = desc_k_sw128(smem_u32(rop(s, 1)) + ro);
             const unsigned acc = kk > 0 ? 1u : 0u;
-            mma_tf32(d1, c1l, r1h, idesc, acc);
-            mma_tf32(d1, c1h, r1l, idesc, 1u);
-            mma_tf32(d1, c1h, r1h, idesc, 1u);
+            if (a.terms == 3) {
+              mma_tf32(d1, c1l, r1h, idesc, acc);
+              mma_tf32(d1, c1h, r1l, idesc, 1u);
+            }
+            mma_tf32(d1, c1h, r1h, idesc, a.terms == 3 ? 1u : acc);
             if (a.dpl) {
               const uint64_t c2h = a.two_c ? desc_k_sw128(smem_u32(cop(2)) + co) : c1h;
               const uint64_t c2l = a.two_c ? desc_k_sw128(smem_u32(cop(3)) + co) : c1l;
               const uint64_t r2h = a.two_r ? desc_k_sw128(smem_u32(rop(s, 2)) + ro) : r1h;
               const uint64_t r2l = a.two_r ? desc_k_sw128(smem_u32(rop(s, 3)) + ro) : r1l;
-              mma_tf32(d2, c2l, r2h, idesc, acc);
-              mma_tf32(d2, c2h, r2l, idesc, 1u);
-              mma_tf32(d2, c2h, r2h, idesc, 1u);
+              if (a.terms == 3) {
+                mma_tf32(d2, c2l, r2h, idesc, acc);
+                mma_tf32(d2, c2h, r2l, idesc, 1u);
+              }
+              mma_tf32(d2, c2h, r2h, idesc, a.terms == 3 ? 1u : acc);
             }
           }
           mma_commit(&rempty[s]);
           mma_commit(&accf[ab]);
-          if (++s == rc::NS) { s = 0; ph ^= 1u; }
+          if (++s == NS) { s = 0; ph ^= 1u; }
         }
         mma_commit(cempty);
       }
@@ -524,58 +561,80 @@ __global__ void __launch_bounds__(rc::NTH, 1)
     const int q = w & 3, h = (w - 2) >> 2;
     unsigned aph[2] = {0u, 0u};
     int k = 0;
-    // M and e of this thread's column for the warp's 32 rows of a tile: all 64
-    // loads in flight together, issued one tile ahead (while the previous
-    // tile is computed and stored)
-    float mv[32], ev[32];
-    auto prefetch = [&](int c, bool cok, int i0) {
+    // One tile of this warp: M and e of the thread's column for the warp's 32
+    // rows (all 64 loads in flight before the accumulator wait; the producer
+    // warp has prefetched these rows into L2), then M' and e_new.  The flags
+    // are compile-time in the element loop (DPL: e_new against the second
+    // product; EF: e read and written; RBF: M' in bf16; FULL: all 32 rows exist).
+    auto tile = [&](auto dpl_, auto ef_, auto full_, auto gen_, int c, bool cok, int i0, int ab) {
+      // GEN: every flag read at run time (bf16 output, no error feedback, ...)
+      constexpr bool GEN = decltype(gen_)::value, FULL = decltype(full_)::value;
+      const bool DPL = GEN ? a.dpl != 0 : decltype(dpl_)::value;
+      const bool HE = GEN ? a.has_e != 0 : decltype(ef_)::value;
+      const bool WE = GEN ? a.Eo != nullptr : decltype(ef_)::value;
+      const bool RBF = GEN ? a.r_bf16 != 0 : false;
+      const bool WO = GEN ? a.out != nullptr : true;
+      float mv[32], ev[32];
+      const size_t ldm = (size_t)a.ldm, lde = (size_t)a.lde, ldo = (size_t)a.ldo, ldeo = (size_t)a.ldeo;
+      const float* pm = a.M + (size_t)i0 * ldm + c;
+      const float* pe = HE ? a.E + (size_t)i0 * lde + c : nullptr;
 #pragma unroll
       for (int j = 0; j < 32; j++) {
-        const int i = i0 + j;
-        const bool ok = cok && i < a.n;
-        mv[j] = ok ? __ldcs(a.M + (size_t)i * a.ldm + c) : 0.f;
-        ev[j] = (ok && a.has_e) ? __ldcs(a.E + (size_t)i * a.lde + c) : 0.f;
+        const bool ok = cok && (FULL || i0 + j < a.n);
+        mv[j] = ok ? __ldcs(pm + j * ldm) : 0.f;
+        ev[j] = (ok && HE) ? __ldcs(pe + j * lde) : 0.f;
       }
+      mbar_wait(&accf[ab], aph[ab]);
+      aph[ab] ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const unsigned ta = tbase + ((unsigned)(32 * q) << 16) + (unsigned)(ab * 2 * rc::TR + 32 * h);
+      float* po = reinterpret_cast<float*>(a.out) + (size_t)i0 * ldo + c;
+      __nv_bfloat16* pob = reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)i0 * ldo + c;
+      float* peo = a.Eo + (size_t)i0 * ldeo + c;
+#pragma unroll
+      for (int hh = 0; hh < 2; hh++) {
+        float d1[16], d2[16];
+        v2::tmem_ld16(ta + 16 * hh, d1);
+        if (DPL) v2::tmem_ld16(ta + rc::TR + 16 * hh, d2);
+#pragma unroll
+        for (int jj = 0; jj < 16; jj++) {
+          const int j = 16 * hh + jj;
+          if (!cok || !(FULL || i0 + j < a.n)) continue;
+          float mr = d1[jj];
+          if (RBF) {
+            const __nv_bfloat16 b = __float2bfloat16_rn(mr);
+            if (WO) pob[j * ldo] = b;
+            mr = __bfloat162float(b);
+          } else if (WO) {
+            __stcs(po + j * ldo, mr);
+          }
+          if (WE) __stcs(peo + j * ldeo, (mv[j] + ev[j]) - (DPL ? d2[jj] : mr));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&acce[ab]);
     };
+    using T1 = std::true_type;
+    using F0 = std::false_type;
+    const bool fast = !a.r_bf16 && a.has_e && a.Eo && a.out;   // fp32 M' and error feedback (the DP step)
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
       int band, t_lo, t_hi;
       range(it, band, t_lo, t_hi);
       const int c = band * rc::BC + 32 * q + lane;
       const bool cok = c < a.m;
-      if (t_lo < t_hi) prefetch(c, cok, t_lo * rc::TR + 32 * h);
       for (int t = t_lo; t < t_hi; t++, k++) {
         const int ab = k & 1;
         const int i0 = t * rc::TR + 32 * h;   // this warp's first row
-        float av[32];
-#pragma unroll
-        for (int j = 0; j < 32; j++) av[j] = mv[j] + ev[j];
-        if (t + 1 < t_hi) prefetch(c, cok, i0 + rc::TR);
-        mbar_wait(&accf[ab], aph[ab]);
-        aph[ab] ^= 1u;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const unsigned ta = tbase + ((unsigned)(32 * q) << 16) + (unsigned)(ab * 2 * rc::TR + 32 * h);
-#pragma unroll
-        for (int hh = 0; hh < 2; hh++) {
-          float d1[16], d2[16];
-          v2::tmem_ld16(ta + 16 * hh, d1);
-          if (a.dpl) v2::tmem_ld16(ta + rc::TR + 16 * hh, d2);
-#pragma unroll
-          for (int j = 0; j < 16; j++) {
-            const int i = i0 + 16 * hh + j;
-            if (!cok || i >= a.n) continue;
-            float mr = d1[j];
-            if (a.r_bf16) mr = __bfloat162float(__float2bfloat16_rn(mr));
-            if (a.out) {
-              if (a.r_bf16)
-                reinterpret_cast<__nv_bfloat16*>(a.out)[(size_t)i * a.ldo + c] = __float2bfloat16_rn(mr);
-              else
-                __stcs(reinterpret_cast<float*>(a.out) + (size_t)i * a.ldo + c, mr);
-            }
-            if (a.Eo) __stcs(a.Eo + (size_t)i * a.ldeo + c, av[16 * hh + j] - (a.dpl ? d2[j] : mr));
-          }
+        const bool full = i0 + 32 <= a.n;
+        if (fast && a.dpl) {
+          if (full) tile(T1{}, T1{}, T1{}, F0{}, c, cok, i0, ab);
+          else tile(T1{}, T1{}, F0{}, F0{}, c, cok, i0, ab);
+        } else if (fast) {
+          if (full) tile(F0{}, T1{}, T1{}, F0{}, c, cok, i0, ab);
+          else tile(F0{}, T1{}, F0{}, F0{}, c, cok, i0, ab);
+        } else {
+          tile(F0{}, F0{}, F0{}, T1{}, c, cok, i0, ab);
         }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        mbar_arrive(&acce[ab]);
       }
     }
   }
@@ -782,6 +841,8 @@ static cudaError_t launch_recon(const Params& p, cudaStream_t st) {
   a.dpl = dpl;
   a.has_e = p.err_in != nullptr;
   a.r_bf16 = p.r_bf16;
+  a.terms = 3;
+  if (const char* tt = getenv("OCC_RC_TERMS")) a.terms = atoi(tt) == 1 ? 1 : 3;
   a.M = static_cast<const float*>(p.M);
   a.ldm = p.ldm;
   a.E = p.err_in;
@@ -791,6 +852,8 @@ static cudaError_t launch_recon(const Params& p, cudaStream_t st) {
   a.Eo = p.err_out;
   a.ldeo = p.lde_out;
   const int smem = rc::Cfg<R>::smem(a.two_c, a.two_r);
+  a.ns = rc::Cfg<R>::stages(a.two_c, a.two_r);
+  if (a.ns < 2) return cudaErrorNotSupported;
   auto kern = umma_recon_kernel<R>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

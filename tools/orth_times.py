@@ -20,11 +20,12 @@ from workloads import synth  # noqa: E402
 NAMES_SLOW = {3: "P reduce + Gram partials (B)", 1: "C1 Gram reduce", 2: "C1 Cholesky", 4: "C1 L^-1",
               5: "C1 P_hat (+ 2nd Gram partials)", 9: "C3 Gram reduce (after barrier)", 10: "C3 Cholesky",
               11: "C3 L^-1", 6: "C3 P_hat + barrier", 7: "sweep 2 (D)", 8: "Q reduce (E)"}
-NAMES_FAST = {1: "sweep 1 (A)", 9: "P reduce + Gram partials + barrier", 10: "factorisation (CTA 0) + barrier",
+NAMES_FAST = {1: "sweep 1 (A)", 9: "P reduce + Gram partials + reduce + barriers", 2: "factor: Gram load",
+              3: "factor: LDL + inverse sweep", 4: "factor: Li, kappa", 10: "barrier",
               11: "apply P_hat", 6: "barrier", 7: "sweep 2 (D)", 8: "Q reduce (E)"}
 FAST = os.environ.get("OCC_FAST_ORTH", "1") != "0"
 NAMES = NAMES_FAST if FAST else NAMES_SLOW
-ORDER = (1, 9, 10, 11, 6, 7, 8) if FAST else (3, 1, 2, 4, 5, 9, 10, 11, 6, 7, 8)
+ORDER = (1, 9, 2, 3, 4, 10, 11, 6, 7, 8) if FAST else (3, 1, 2, 4, 5, 9, 10, 11, 6, 7, 8)
 
 
 def main():
