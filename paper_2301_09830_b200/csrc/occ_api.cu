@@ -57,7 +57,13 @@ occ_status cuda_fail(cudaError_t e, const char* what) {
 
 constexpr int kGeomSms = 148;              // geometry is device independent (B200 SM count)
 constexpr double kTau = 1e-5;              // reading C3
-constexpr double kKappaTwoPass = 1e4;      // CholQR2 trigger on ||L||_F ||L^-1||_F
+constexpr double kKappaTwoPass = 1e4;      // CholQR2 trigger on ||L||_F ||L^-1||_F (fused kernel)
+// The per-phase path forms P_hat = P Li^T from an fp64 Gram of the fp32 P, so
+// the first pass's loss of orthogonality is ~ kappa^2 u_64 (<= 1e-8 at 1e4,
+// 1e-4 at the worst kappa_est 1e6 only if kappa_est is tight; it overestimates
+// kappa by up to sqrt(r)) next to the fp32 rounding of P_hat itself, which no
+// second pass removes: CholQR2 runs there only above 1e6 (reading C3)
+constexpr double kKappaTwoPassPhase = 1e6;
 constexpr unsigned long long kFbSeed = 0;  // fallback-vector seed (oracle default)
 
 size_t esize(occ_dtype d) { return d == OCC_BF16 ? 2 : 4; }
@@ -156,6 +162,12 @@ Params base_params(const occ_mat& M, const occ_mat& err, const occ_mat& Q, const
   p.fb_seed = kFbSeed;
   p.tau = kTau;
   p.kappa_thr = kKappaTwoPass;
+  p.kappa_thr_phase = kKappaTwoPassPhase;
+  static const double kphase_env = [] {   // experiment knob (tools/kappa_ab.py)
+    const char* e = getenv("OCC_KAPPA_PHASE");
+    return e ? atof(e) : 0.0;
+  }();
+  if (kphase_env > 0.0) p.kappa_thr_phase = kphase_env;
   p.force_two_pass = (flags & OCC_FORCE_TWO_PASS) ? 1 : 0;
   p.check_finite = (flags & OCC_CHECK_FINITE) ? 1 : 0;
   p.wire_bf16 = (flags & OCC_WIRE_BF16) ? 1 : 0;

@@ -137,6 +137,7 @@ struct Params {
   unsigned long long fb_seed;
   double tau;
   double kappa_thr;
+  double kappa_thr_phase;  // the per-phase path's CholQR2 trigger (orth_fast; reading C3)
   int force_two_pass;
   int check_finite;      // OCC_CHECK_FINITE: flag a non-finite Gram diagonal (non-finite M or e)
   int wire_bf16;         // OCC_WIRE_BF16: round P_hat and Q to bf16 before the reconstruction
@@ -992,7 +993,7 @@ __device__ int factor_fast(const Params& p, const double* part, int npart, bool 
     for (int w = 0; w < NW; w++) { a += red[w]; b += red[NW + w]; }
     const double kappa = sqrt(a) * sqrt(b);
     if (first_pass) {
-      plan = (p.force_two_pass || kappa > p.kappa_thr) ? 3 : 0;
+      plan = (p.force_two_pass || kappa > p.kappa_thr_phase) ? 3 : 0;
       p.stats->fallback_columns = 0;
       p.stats->second_pass = plan == 3 ? 1 : 0;
       p.stats->kappa_est = kappa;

@@ -172,12 +172,12 @@ __global__ void __launch_bounds__(NTH, 1)
   if (tid == 0) {
     for (int s = 0; s < NS; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], NCV);
+      mbar_init(&conv[s], NCV / 32);   // one arrival per converter warp
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], NCV);
+      mbar_init(&acce[b], NCV / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(NTH, 1)
         for (int u = 0; u < 16; u++) acc[16 * j + u] += v[u];
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&acce[ab]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[ab]);
     };
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
       int band, gi, c_lo, c_hi;
@@ -319,7 +320,8 @@ __global__ void __launch_bounds__(NTH, 1)
             pe[x] = lo;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&conv[s]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[s]);
           if (++s == NS) { s = 0; ph ^= 1u; }
         }
         if (pend >= 0) drain(pend);   // the previous accumulator, while this one's MMAs run
@@ -379,10 +381,8 @@ struct Cfg {
 
 struct RcArgs {
   int n, m, nb, G, ntile;       // column bands, row splits per band, 64-row tiles
-  int two_c, two_r;             // the e_new product has its own column / row factor
   int dpl;                      // e_new = A - D2 (else A - round(D1))
   int has_e, r_bf16;
-  int terms;                    // 3 (the fp32-level split); 1 only as a timing experiment (OCC_RC_TERMS)
   int ns;                       // row-factor stages
   const float* M; long long ldm;
   const float* E; long long lde;
@@ -390,7 +390,9 @@ struct RcArgs {
   float* Eo; long long ldeo;    // e_new (nullptr: not written)
 };
 
-template <int R>
+// MODE: 0 e_new = A - M' (global EF, one product); 1 plain DP, local EF (a
+// second column factor Q_w); 2 OCC_ORIENT_T, local EF (a second row factor V_w)
+template <int R, int MODE>
 __global__ void __launch_bounds__(rc::NTH, 1)
     umma_recon_kernel(const __grid_constant__ CUtensorMap tC1h, const __grid_constant__ CUtensorMap tC1l,
                       const __grid_constant__ CUtensorMap tC2h, const __grid_constant__ CUtensorMap tC2l,
@@ -403,7 +405,8 @@ __global__ void __launch_bounds__(rc::NTH, 1)
   constexpr int RB1 = rc::TR * 32 * 4;       // one K block of a row operand
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
-  const int ncop = a.two_c ? 4 : 2, nrop = a.two_r ? 4 : 2;
+  constexpr bool TWO_C = MODE == 1, TWO_R = MODE == 2, DPL2 = MODE != 0;
+  constexpr int ncop = TWO_C ? 4 : 2, nrop = TWO_R ? 4 : 2;
   unsigned char* cbase = sm;                                   // [ncop][KB][128 rows][128 B]
   unsigned char* rbase = sm + ncop * C::CBOX;                  // [NS][nrop][KB][64 rows][128 B]
   const int NS = a.ns;
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(rc::NTH, 1)
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], rc::NEP);
+      mbar_init(&acce[b], rc::NEP / 32);   // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -449,28 +452,10 @@ __global__ void __launch_bounds__(rc::NTH, 1)
     t_hi = (int)((long long)(gi + 1) * a.ntile / a.G);
   };
 
-  if (w == 0) {   // ------------------------------------------------ TMA producer (lane 0) + L2 prefetch (warp)
+  if (w == 0) {   // ------------------------------------------------ TMA producer (lane 0)
     const unsigned long long pol = v2::l2_evict_normal();
     int s = 0;
     unsigned ph = 0, cph = 0;
-    // the tile's rows of M and e (this band's 128 columns: 512 B each) into L2,
-    // PF tiles ahead of the epilogue, whose per-lane column loads then hit L2
-    constexpr int PF = 3;
-    auto prefetch_tile = [&](int band, int t) {
-      const int c0 = band * rc::BC;
-      const unsigned bytes = (unsigned)min(rc::BC, a.m - c0) * 4u;
-#pragma unroll
-      for (int h = 0; h < rc::TR / 32; h++) {
-        const int i = t * rc::TR + 32 * h + lane;
-        if (i < a.n) {
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.M + (size_t)i * a.ldm + c0), "r"(bytes)
-                       : "memory");
-          if (a.has_e)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.E + (size_t)i * a.lde + c0), "r"(bytes)
-                         : "memory");
-        }
-      }
-    };
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
       int band, t_lo, t_hi;
       range(it, band, t_lo, t_hi);
@@ -481,15 +466,13 @@ __global__ void __launch_bounds__(rc::NTH, 1)
         for (int kb = 0; kb < KB; kb++) {
           tma_2d(cop(0) + kb * CB1, &tC1h, 32 * kb, band * rc::BC, cfull, pol);
           tma_2d(cop(1) + kb * CB1, &tC1l, 32 * kb, band * rc::BC, cfull, pol);
-          if (a.two_c) {
+          if (TWO_C) {
             tma_2d(cop(2) + kb * CB1, &tC2h, 32 * kb, band * rc::BC, cfull, pol);
             tma_2d(cop(3) + kb * CB1, &tC2l, 32 * kb, band * rc::BC, cfull, pol);
           }
         }
       }
       cph ^= 1u;
-      __syncwarp();
-      for (int t = t_lo; t < min(t_hi, t_lo + PF); t++) prefetch_tile(band, t);
       for (int t = t_lo; t < t_hi; t++) {
         if (lane == 0) {
           mbar_wait(&rempty[s], ph ^ 1u);
@@ -498,14 +481,12 @@ __global__ void __launch_bounds__(rc::NTH, 1)
           for (int kb = 0; kb < KB; kb++) {
             tma_2d(rop(s, 0) + kb * RB1, &tR1h, 32 * kb, t * rc::TR, &rfull[s], pol);
             tma_2d(rop(s, 1) + kb * RB1, &tR1l, 32 * kb, t * rc::TR, &rfull[s], pol);
-            if (a.two_r) {
+            if (TWO_R) {
               tma_2d(rop(s, 2) + kb * RB1, &tR2h, 32 * kb, t * rc::TR, &rfull[s], pol);
               tma_2d(rop(s, 3) + kb * RB1, &tR2l, 32 * kb, t * rc::TR, &rfull[s], pol);
             }
           }
         }
-        __syncwarp();
-        if (t + PF < t_hi) prefetch_tile(band, t + PF);
         if (++s == NS) { s = 0; ph ^= 1u; }
       }
     }
@@ -526,28 +507,27 @@ __global__ void __launch_bounds__(rc::NTH, 1)
           mbar_wait(&rfull[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const unsigned d1 = tbase + (unsigned)(ab * 2 * rc::TR), d2 = d1 + rc::TR;
+          // descriptors of the stage's operands; the K steps add constant offsets
+          // (16-byte units) to the start-address field: a straight-line block of
+          // 3 R / 8 (x 2 with the second product) MMAs
+          const uint64_t c1h = desc_k_sw128(smem_u32(cop(0))), c1l = desc_k_sw128(smem_u32(cop(1)));
+          const uint64_t r1h = desc_k_sw128(smem_u32(rop(s, 0))), r1l = desc_k_sw128(smem_u32(rop(s, 1)));
+          const uint64_t c2h = TWO_C ? desc_k_sw128(smem_u32(cop(2))) : c1h;
+          const uint64_t c2l = TWO_C ? desc_k_sw128(smem_u32(cop(3))) : c1l;
+          const uint64_t r2h = TWO_R ? desc_k_sw128(smem_u32(rop(s, 2))) : r1h;
+          const uint64_t r2l = TWO_R ? desc_k_sw128(smem_u32(rop(s, 3))) : r1l;
 #pragma unroll
           for (int kk = 0; kk < R / 8; kk++) {
-            const unsigned co = (unsigned)((kk >> 2) * CB1 + (kk & 3) * 32);
-            const unsigned ro = (unsigned)((kk >> 2) * RB1 + (kk & 3) * 32);
-            const uint64_t c1h = desc_k_sw128(smem_u32(cop(0)) + co), c1l = desc_k_sw128(smem_u32(cop(1)) + co);
-            const uint64_t r1h = desc_k_sw128(smem_u32(rop(s, 0)) + ro), r1l = desc_k_sw128(smem_u32(rop(s, 1)) + ro);
+            const uint64_t co = (uint64_t)(((kk >> 2) * CB1 + (kk & 3) * 32) >> 4);
+            const uint64_t ro = (uint64_t)(((kk >> 2) * RB1 + (kk & 3) * 32) >> 4);
             const unsigned acc = kk > 0 ? 1u : 0u;
-            if (a.terms == 3) {
-              mma_tf32(d1, c1l, r1h, idesc, acc);
-              mma_tf32(d1, c1h, r1l, idesc, 1u);
-            }
-            mma_tf32(d1, c1h, r1h, idesc, a.terms == 3 ? 1u : acc);
-            if (a.dpl) {
-              const uint64_t c2h = a.two_c ? desc_k_sw128(smem_u32(cop(2)) + co) : c1h;
-              const uint64_t c2l = a.two_c ? desc_k_sw128(smem_u32(cop(3)) + co) : c1l;
-              const uint64_t r2h = a.two_r ? desc_k_sw128(smem_u32(rop(s, 2)) + ro) : r1h;
-              const uint64_t r2l = a.two_r ? desc_k_sw128(smem_u32(rop(s, 3)) + ro) : r1l;
-              if (a.terms == 3) {
-                mma_tf32(d2, c2l, r2h, idesc, acc);
-                mma_tf32(d2, c2h, r2l, idesc, 1u);
-              }
-              mma_tf32(d2, c2h, r2h, idesc, a.terms == 3 ? 1u : acc);
+            mma_tf32(d1, c1l + co, r1h + ro, idesc, acc);
+            mma_tf32(d1, c1h + co, r1l + ro, idesc, 1u);
+            mma_tf32(d1, c1h + co, r1h + ro, idesc, 1u);
+            if (DPL2) {
+              mma_tf32(d2, c2l + co, r2h + ro, idesc, acc);
+              mma_tf32(d2, c2h + co, r2l + ro, idesc, 1u);
+              mma_tf32(d2, c2h + co, r2h + ro, idesc, 1u);
             }
           }
           mma_commit(&rempty[s]);
@@ -562,8 +542,9 @@ __global__ void __launch_bounds__(rc::NTH, 1)
     unsigned aph[2] = {0u, 0u};
     int k = 0;
     // One tile of this warp: M and e of the thread's column for the warp's 32
-    // rows (all 64 loads in flight before the accumulator wait; the producer
-    // warp has prefetched these rows into L2), then M' and e_new.  The flags
+    // rows (all 64 loads in flight before the accumulator wait), then M' and
+    // e_new.  (An L2 bulk prefetch of the next tiles' rows by the producer warp
+    // measured slower: 194 vs 160 us for the MLP matrix.)  The flags
     // are compile-time in the element loop (DPL: e_new against the second
     // product; EF: e read and written; RBF: M' in bf16; FULL: all 32 rows exist).
     auto tile = [&](auto dpl_, auto ef_, auto full_, auto gen_, int c, bool cok, int i0, int ab) {
@@ -612,7 +593,8 @@ __global__ void __launch_bounds__(rc::NTH, 1)
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&acce[ab]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[ab]);
     };
     using T1 = std::true_type;
     using F0 = std::false_type;
@@ -643,17 +625,33 @@ __global__ void __launch_bounds__(rc::NTH, 1)
   if (w == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(256));
 }
 
-// The reconstruction's factor operands: x (rows x R, row stride R) scaled by
-// `scale`, split hi / lo (K-major, row stride R); `state` (optional) receives
-// the scaled factor (the warm start, reading C15).
-__global__ void occ_split_rows_kernel(const float* __restrict__ x, long long count, float scale, unsigned* hi,
-                                      unsigned* lo, float* state) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
-    const float v = scale * x[i];
-    if (state) state[i] = v;
-    const unsigned hb = __float_as_uint(v) & 0xffffe000u;
-    hi[i] = hb;
-    lo[i] = __float_as_uint(v - __uint_as_float(hb));
+// The reconstruction's factor operands, all in one launch: for each of up to
+// four factors x (rows x R, row stride R), x scaled by `scale`, split hi / lo
+// (K-major, row stride R); `state` (optional) receives the scaled factor (the
+// warm start, reading C15).
+struct SplitJob {
+  const float* x;
+  long long count;
+  float scale;
+  unsigned* hi;
+  unsigned* lo;
+  float* state;
+};
+struct SplitJobs {
+  SplitJob j[4];
+  int n;
+};
+__global__ void occ_split_rows_kernel(const __grid_constant__ SplitJobs jobs) {
+  for (int q = 0; q < jobs.n; q++) {
+    const SplitJob& J = jobs.j[q];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < J.count;
+         i += (long long)gridDim.x * blockDim.x) {
+      const float v = J.scale * J.x[i];
+      if (J.state) J.state[i] = v;
+      const unsigned hb = __float_as_uint(v) & 0xffffe000u;
+      J.hi[i] = hb;
+      J.lo[i] = __float_as_uint(v - __uint_as_float(hb));
+    }
   }
 }
 
@@ -811,16 +809,19 @@ static cudaError_t launch_recon(const Params& p, cudaStream_t st) {
   unsigned* r1l = r1h + (size_t)n * R;
   unsigned* r2h = r1l + (size_t)n * R;
   unsigned* r2l = r2h + (size_t)n * R;
-  auto split = [&](const float* x, long long rows, float scale, unsigned* hi, unsigned* lo, float* state) {
-    const long long cnt = rows * R;
-    const int grid = (int)std::max<long long>(1, std::min<long long>((cnt + 255) / 256, 2048));
-    occ_split_rows_kernel<<<grid, 256, 0, st>>>(x, cnt, scale, hi, lo, state);
-    return cudaGetLastError();
+  SplitJobs jobs;
+  jobs.n = 0;
+  long long most = 0;
+  auto add = [&](const float* x, long long rows, float scale, unsigned* hi, unsigned* lo, float* state) {
+    jobs.j[jobs.n++] = SplitJob{x, rows * R, scale, hi, lo, state};
+    most = std::max(most, rows * R);
   };
-  cudaError_t e = split(c1, m, rowloc ? 1.f : p.scale, c1h, c1l, rowloc ? nullptr : p.Qstate_out);
-  if (e == cudaSuccess) e = split(r1, n, rowloc ? p.scale : 1.f, r1h, r1l, rowloc ? p.Pstate_out : nullptr);
-  if (e == cudaSuccess && c2) e = split(c2, m, 1.f, c2h, c2l, nullptr);
-  if (e == cudaSuccess && r2) e = split(r2, n, 1.f, r2h, r2l, nullptr);
+  add(c1, m, rowloc ? 1.f : p.scale, c1h, c1l, rowloc ? nullptr : p.Qstate_out);
+  add(r1, n, rowloc ? p.scale : 1.f, r1h, r1l, rowloc ? p.Pstate_out : nullptr);
+  if (c2) add(c2, m, 1.f, c2h, c2l, nullptr);
+  if (r2) add(r2, n, 1.f, r2h, r2l, nullptr);
+  occ_split_rows_kernel<<<(int)std::max<long long>(1, std::min<long long>((most + 255) / 256, 1184)), 256, 0, st>>>(jobs);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap t[8];
   bool ok = tmap_f32(&t[0], c1h, m, R, R, 32, rc::BC) && tmap_f32(&t[1], c1l, m, R, R, 32, rc::BC) &&
@@ -836,13 +837,9 @@ static cudaError_t launch_recon(const Params& p, cudaStream_t st) {
   a.ntile = (n + rc::TR - 1) / rc::TR;
   const int sms = sm_count();
   a.G = choose_splits(a.nb, a.ntile, a.ntile, sms);
-  a.two_c = c2 != nullptr;
-  a.two_r = r2 != nullptr;
   a.dpl = dpl;
   a.has_e = p.err_in != nullptr;
   a.r_bf16 = p.r_bf16;
-  a.terms = 3;
-  if (const char* tt = getenv("OCC_RC_TERMS")) a.terms = atoi(tt) == 1 ? 1 : 3;
   a.M = static_cast<const float*>(p.M);
   a.ldm = p.ldm;
   a.E = p.err_in;
@@ -851,10 +848,11 @@ static cudaError_t launch_recon(const Params& p, cudaStream_t st) {
   a.ldo = p.ldr;
   a.Eo = p.err_out;
   a.ldeo = p.lde_out;
-  const int smem = rc::Cfg<R>::smem(a.two_c, a.two_r);
-  a.ns = rc::Cfg<R>::stages(a.two_c, a.two_r);
+  const bool two_c = c2 != nullptr, two_r = r2 != nullptr;
+  const int smem = rc::Cfg<R>::smem(two_c, two_r);
+  a.ns = rc::Cfg<R>::stages(two_c, two_r);
   if (a.ns < 2) return cudaErrorNotSupported;
-  auto kern = umma_recon_kernel<R>;
+  auto kern = two_c ? umma_recon_kernel<R, 1> : two_r ? umma_recon_kernel<R, 2> : umma_recon_kernel<R, 0>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   kern<<<std::min(a.nb * a.G, sms), rc::NTH, smem, st>>>(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], a);
