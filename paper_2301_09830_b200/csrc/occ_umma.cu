@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(rc::NTH, 1)
     // measured slower: 194 vs 160 us for the MLP matrix.)  The flags
     // are compile-time in the element loop (DPL: e_new against the second
     // product; EF: e read and written; RBF: M' in bf16; FULL: all 32 rows exist).
-    auto tile = [&](auto dpl_, auto ef_, auto full_, auto gen_, int c, bool cok, int i0, int ab) {
+    auto tile = [&](auto dpl_, auto ef_, auto full_, auto gen_, int c, bool cok, int i0, int ab, int inext) {
       // GEN: every flag read at run time (bf16 output, no error feedback, ...)
       constexpr bool GEN = decltype(gen_)::value, FULL = decltype(full_)::value;
       const bool DPL = GEN ? a.dpl != 0 : decltype(dpl_)::value;
@@ -564,6 +564,13 @@ __global__ void __launch_bounds__(rc::NTH, 1)
         const bool ok = cok && (FULL || i0 + j < a.n);
         mv[j] = ok ? __ldcs(pm + j * ldm) : 0.f;
         ev[j] = (ok && HE) ? __ldcs(pe + j * lde) : 0.f;
+      }
+      // the warp's next tile into L2 while this one waits and stores: lane j
+      // prefetches the 128-byte line of row inext + j (the warp's 32 columns)
+      if (inext >= 0 && inext + lane < a.n && c - lane < a.m) {
+        const size_t o = (size_t)(inext + lane);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.M + o * ldm + (c - lane)));
+        if (HE) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.E + o * lde + (c - lane)));
       }
       mbar_wait(&accf[ab], aph[ab]);
       aph[ab] ^= 1u;
@@ -608,14 +615,15 @@ __global__ void __launch_bounds__(rc::NTH, 1)
         const int ab = k & 1;
         const int i0 = t * rc::TR + 32 * h;   // this warp's first row
         const bool full = i0 + 32 <= a.n;
+        const int inext = t + 1 < t_hi ? i0 + rc::TR : -1;
         if (fast && a.dpl) {
-          if (full) tile(T1{}, T1{}, T1{}, F0{}, c, cok, i0, ab);
-          else tile(T1{}, T1{}, F0{}, F0{}, c, cok, i0, ab);
+          if (full) tile(T1{}, T1{}, T1{}, F0{}, c, cok, i0, ab, inext);
+          else tile(T1{}, T1{}, F0{}, F0{}, c, cok, i0, ab, inext);
         } else if (fast) {
-          if (full) tile(F0{}, T1{}, T1{}, F0{}, c, cok, i0, ab);
-          else tile(F0{}, T1{}, F0{}, F0{}, c, cok, i0, ab);
+          if (full) tile(F0{}, T1{}, T1{}, F0{}, c, cok, i0, ab, inext);
+          else tile(F0{}, T1{}, F0{}, F0{}, c, cok, i0, ab, inext);
         } else {
-          tile(F0{}, F0{}, F0{}, T1{}, c, cok, i0, ab);
+          tile(F0{}, F0{}, F0{}, T1{}, c, cok, i0, ab, inext);
         }
       }
     }
