@@ -509,7 +509,9 @@ static Plan2 plan_search(int64_t n, int64_t m, int sms, bool mbf) {
   constexpr int RP = K<R>::RP, MT = K<R>::MT, KS5 = K<R>::KS5, NP = K<R>::NP;
   Plan2 best;
   const int smem_cap = 227 * 1024 - 2048;
+  const char* force_nc = getenv("OCC_V2_NC");   // experiment knob: only plans with this column-tile count
   for (int nc = 1; nc <= sms; nc++) {
+    if (force_nc && nc != atoi(force_nc)) continue;
     const int nr_max = sms / nc;
     if (nr_max < 1) break;
     const int W = (int)(((m + nc - 1) / nc + 15) / 16 * 16);

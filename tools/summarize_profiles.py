@@ -3,7 +3,8 @@
 share of the listed time) and the key metrics of the --set full capture of
 the fused kernel; also refreshes profiles/traffic.json, which bench.py reads.
 
-    python tools/summarize_profiles.py [round-tag]     (default: round1)
+    python tools/summarize_profiles.py [round-tag] [raw-prefix]   (default: round2b r2g,
+    the outputs of tools/round2b_profile.sh)
 """
 import csv
 import io
@@ -78,6 +79,9 @@ def ncu_kernels(rep, match):
         if match in d.get("Kernel Name", ""):
             x = {"kernel": d["Kernel Name"]}
             for k in METRICS + ["sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+                                "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                                "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                                "dram__throughput.avg.pct_of_peak_sustained_elapsed",
                                 "smsp__average_warp_latency_per_inst_issued.ratio"]:
                 v = d.get(k)
                 try:
@@ -89,8 +93,8 @@ def ncu_kernels(rep, match):
 
 
 def main():
-    tag = sys.argv[1] if len(sys.argv) > 1 else "round2"
-    pre = os.path.join(RAW, "r2f")
+    tag = sys.argv[1] if len(sys.argv) > 1 else "round2b"
+    pre = os.path.join(RAW, sys.argv[2] if len(sys.argv) > 2 else "r2g")
     os.makedirs(OUT, exist_ok=True)
     res = {}
     for name in ("bench_n1", "bench_C3", "bench_C4", "bench_ref"):
@@ -103,25 +107,35 @@ def main():
             json.dump(d, open(os.path.join(OUT, f"{tag}_{name.replace('bench_ref', 'bench_reference')}.json"), "w"),
                       indent=1)
             res[name] = d.get("ms_per_step")
-    f = f"{pre}_launches_n1.csv"
-    if os.path.exists(f):
+    for lname in ("n1", "C3", "C4"):
+        f = f"{pre}_launches_{lname}.csv"
+        if not os.path.exists(f):
+            continue
         ll = launches(f)
-        with open(os.path.join(OUT, f"{tag}_launches_n1.csv"), "w") as fo:
+        with open(os.path.join(OUT, f"{tag}_launches_{lname}.csv"), "w") as fo:
             w = csv.writer(fo)
             w.writerow(["kernel", "launches", "mean_us", "share_of_listed_time"])
             for x in ll:
                 w.writerow([x["kernel"], x["launches"], x["mean_us"], x["share_of_listed_time"]])
-        res["launches"] = ll[:4]
+        res["launches_" + lname] = ll[:6]
+    f = f"{pre}_pytest_gpu.log"
+    if os.path.exists(f):
+        with open(os.path.join(OUT, f"{tag}_pytest_gpu.log"), "w") as fo:
+            fo.write(open(f).read())
     caps = {"v2_C2": ("occ_v2_kernel", "bench.py --config C2"), "v2_T": ("occ_v2_kernel", "bench.py --config T"),
             "phaseA_C3": ("occ_step_kernel", "big_phase_times multi, launch 0"),
             "phaseD_C3": ("occ_step_kernel", "big_phase_times multi, launch 5"),
             "decompress_C3": ("occ_v2_decompress_band", "big_phase_times multi, EF + plain"),
-            "phaseF_C4": ("occ_step_kernel", "big_phase_times multi, launch 30 (DP reconstruction, MLP)")}
+            "phaseF_C4": ("occ_step_kernel", "big_phase_times multi, launch 30 (DP reconstruction, MLP)"),
+            "sweep1_C4": ("umma_sweep_kernel", "tools/dp_driver.py: tcgen05 sweep 1, 3072x12288 r64"),
+            "sweep2_C4": ("umma_sweep_kernel", "tools/dp_driver.py: tcgen05 sweep 2 (MN-major A), 3072x12288 r64"),
+            "recon_C4": ("umma_recon_kernel", "tools/dp_driver.py: tcgen05 DP reconstruction, 3072x12288 r64"),
+            "orth_C4": ("occ_step_kernel", "tools/dp_driver.py: Gram + one-CTA factorisation + apply, 3072x12288 r64")}
     ncu = {}
     for key, (match, how) in caps.items():
         rep = f"{pre}_{key}.ncu-rep"
         if os.path.exists(rep) or os.path.exists(f"{pre}_{key}.raw.csv"):
-            ncu[key] = {"source": f"ncu --set full --clock-control none --import-source on ({how}); tools/round2_profile.sh",
+            ncu[key] = {"source": f"ncu --set full --clock-control none --import-source on ({how}); tools/round2b_profile.sh",
                         "kernels": ncu_kernels(rep, match)}
     json.dump(ncu, open(os.path.join(OUT, f"{tag}_ncu_full.json"), "w"), indent=1)
     if "v2_C2" in ncu and ncu["v2_C2"]["kernels"]:
