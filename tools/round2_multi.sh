@@ -5,7 +5,7 @@
 set -u
 NG=${1:-2}
 mkdir -p gpurun_out
-o=gpurun_out/r2m_n$NG
+o=gpurun_out/${PREFIX:-r2m}_n$NG
 python -m pytest tests -m gpu -q > ${o}_pytest.log 2>&1; echo "rc=$?" >> ${o}_pytest.log
 for c in C2 C3 C4; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port $((29600 + NG)) \
