@@ -256,6 +256,13 @@ def main():
     snd_peer, rcv_peer = (rank - 1) % world, (rank + 1) % world   # pp ring
     links = []   # occ_link per input set (N > 1 ring with --exchange link)
     use_link = world > 1 and args.exchange == "link" and CONFIGS[args.config]["kind"] != "dp"
+    # DP (C4) with --exchange link: the factor sums in-kernel over NVLink (occ_dplink) at N = 2,
+    # where it measured faster than NCCL (47 vs 56 us for the two sums); its one-shot push
+    # moves (N - 1) buckets per rank, so N > 2 stays on ncclAllReduce (95 vs 63 us at N = 4)
+    dplink = None
+    if world == 2 and args.exchange == "link" and CONFIGS[args.config]["kind"] == "dp":
+        c4 = CONFIGS[args.config]
+        dplink = occ.DpLink.open(comm, max(sum(n for n, _ in c4["shapes"]), sum(m for _, m in c4["shapes"])) * c4["r"])
 
     def flush_l2():
         flush.fill_(1.0)   # write 2x L2: evicts (and writes back) everything before the timed step
@@ -296,9 +303,13 @@ def main():
             M = b["M"] if Min is None else Min
             R = b["R"] if Rout is None else Rout
             if kind == "dp":
-                occ.occ_allreduce_factors([x["M"] for x in mats] if Min is None else [M] + [x["M"] for x in mats[1:]],
-                                          [x["E"] for x in mats], [x["Q"] for x in mats], [x["P"] for x in mats],
-                                          r, 1.0 / world, comm=comm, ws=ws)
+                Gs = [x["M"] for x in mats] if Min is None else [M] + [x["M"] for x in mats[1:]]
+                if dplink is not None:
+                    occ.occ_allreduce_factors_link(Gs, [x["E"] for x in mats], [x["Q"] for x in mats],
+                                                   [x["P"] for x in mats], r, 1.0 / world, dplink, ws=ws)
+                else:
+                    occ.occ_allreduce_factors(Gs, [x["E"] for x in mats], [x["Q"] for x in mats],
+                                              [x["P"] for x in mats], r, 1.0 / world, comm=comm, ws=ws)
                 return M
             if world > 1 and link is not None:
                 occ.occ_sendrecv_factors_link(M, b["E"], b["Q"], b["P"], r, R, b["Pr"], b["Qr"], link, ws=ws)
@@ -435,9 +446,13 @@ def main():
             pb = torch.zeros(sum(n for n, _ in cfg["shapes"]) * r, device=dev)
             qb = torch.zeros(sum(m for _, m in cfg["shapes"]) * r, device=dev)
 
-            def xchg():   # the two NCCL calls of occ_allreduce_factors, on its message sizes
-                dist.all_reduce(pb)
-                dist.all_reduce(qb)
+            def xchg():   # the two factor sums of occ_allreduce_factors(_link), on its bucket sizes
+                if dplink is not None:
+                    dplink.allreduce(pb, pb)
+                    dplink.allreduce(qb, qb)
+                else:
+                    dist.all_reduce(pb)
+                    dist.all_reduce(qb)
         else:
             b = res["sets"][0].mats[0]
             lk = res["sets"][0].link
@@ -516,13 +531,15 @@ def main():
             l1.record(stream)
             barrier()
             local_us = max_over_ranks(l0.elapsed_time(l1) / args.steps * 1e3)
-        comm_line = {"factor_comm_us": comm_us, "exchange": "dp-nccl" if kind == "dp" else args.exchange,
+        comm_line = {"factor_comm_us": comm_us,
+                     "exchange": ("dp-link" if dplink is not None else "dp-nccl") if kind == "dp" else args.exchange,
                      "step_without_exchange_us": local_us,
                      "exchange_cost_in_step_us": None if local_us is None else ms * 1e3 - local_us,
                      "nccl_sendrecv_us": None if kind == "dp" else nccl_us,
                      "factor_bytes": fbytes, "nvlink_busbw_allreduce_GBs": bw["allreduce"],
                      "nvlink_sendrecv_GBs": bw["sendrecv"], "model_us": model_us, "frac_of_nvlink_roofline": model_us / comm_us,
-                     "how": "DP: the two ncclAllReduce calls of occ_allreduce_factors on its bucket sizes; PP: the "
+                     "how": "DP: the two factor sums of the step on its bucket sizes (occ_dplink_allreduce in-kernel over "
+                            "NVLink peer memory with --exchange link, else ncclAllReduce); PP: the "
                             "library's exchange of (P_hat, Q) alone -- occ_sendrecv_factors_link(M=NULL, out=NULL) "
                             "(in-kernel NVLink stores + flag, --exchange link) or occ_sendrecv_factors(M=NULL, "
                             "out=NULL) (grouped NCCL send/recv, also reported as nccl_sendrecv_us); model = "
@@ -563,7 +580,7 @@ def main():
     if rank == 0:
         kern = {"1gpu": "occ_v2_kernel (fused step)" if res["stats"]["path"] == 3 else "per-phase kernels",
                 "pp": "sender compress + receiver decompress kernels" + ("" if world == 1 else (" + in-kernel NVLink exchange" if use_link else " + NCCL send/recv")),
-                "dp": "DP step kernels + 2 NCCL allreduces"}[kind]
+                "dp": "DP step kernels + 2 factor sums" + (" (in-kernel NVLink, occ_dplink)" if dplink is not None else " (NCCL allreduce)")}[kind]
         cd = config_dict(name, world, parallelism)
         cd["l2"] = (f"inputs larger than L2: {res['nsets']} rotating input sets of {elems(cfg) * 12 / 1e6:.0f} MB "
                     f"(M, e, M') back to back; per_step: each step alone after a 2x-L2 write flush")
@@ -594,6 +611,8 @@ def main():
     barrier()
     for lk in links:
         lk.close()
+    if dplink is not None:
+        dplink.close()
     if comm is not None:
         comm.destroy()
     if world > 1:

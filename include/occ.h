@@ -226,6 +226,35 @@ occ_status occ_sendrecv_factors_link(occ_mat M, occ_mat err, occ_mat Q, occ_mat 
                                      occ_mat Qrcv, uint32_t flags, occ_link link, void* ws, size_t ws_bytes,
                                      cudaStream_t stream);
 
+/* In-kernel factor sums of a data-parallel group over NVLink peer memory
+ * (§Impl, the DP allreduce of PowerSGD's
+ * P and Q; reading C1).  occ_dplink_open is collective over `dp` (at most 8
+ * ranks): every rank allocates a mailbox of two slots of max_floats fp32 plus
+ * flag / acknowledgement words, exports it with CUDA IPC and maps every other
+ * member's (handles all-gathered over `dp`).  max_floats bounds the largest
+ * bucket one call sums (the P bucket sum_i rows_i r, or the Q bucket
+ * sum_i cols_i r).
+ * occ_allreduce_factors_link is occ_allreduce_factors (same arguments, layout,
+ * ownership and errors) with each of its two sums done by one kernel instead of
+ * ncclAllReduce: a rank copies its bucket into slot seq % 2 of its own mailbox
+ * and releases its flag (system scope); every rank acquires every member's
+ * flag >= seq, sums the D slots in rank order (so the sum is bit-identical on
+ * every rank) into its output and acknowledges; a slot is rewritten two calls
+ * later, after every member's acknowledgement.  No NCCL call is on this path;
+ * a wait that exceeds ~2 s (peer gone) ends the kernel's wait and
+ * occ_check_status reports OCC_ERR_NCCL.  Every rank of the group must issue
+ * the same sequence of calls.  OCC_ERR_WORKSPACE: a bucket larger than
+ * max_floats. */
+typedef struct occ_dplink_s* occ_dplink;
+occ_status occ_dplink_open(occ_comm dp, int64_t max_floats, occ_dplink* out);
+occ_status occ_dplink_close(occ_dplink link);
+/* The exchange alone: dst[i] = sum over the group of src[i] (count <= max_floats
+ * fp32, 16-byte aligned device pointers, dst may equal src), in rank order. */
+occ_status occ_dplink_allreduce(occ_dplink link, const float* src, float* dst, int64_t count, cudaStream_t stream);
+occ_status occ_allreduce_factors_link(int nmat, const occ_mat* G, const occ_mat* err, const occ_mat* Q, const occ_mat* P,
+                                      const int* r, float scale, uint32_t flags, occ_dplink link, void* ws,
+                                      size_t ws_bytes, cudaStream_t stream);
+
 /* Communicators (NCCL over NVLink / NVSwitch). */
 occ_status occ_get_unique_id(uint8_t id[128]);
 occ_status occ_comm_init(occ_comm* comm, const uint8_t id[128], int nranks, int rank);

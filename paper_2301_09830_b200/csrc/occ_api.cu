@@ -452,10 +452,58 @@ occ_status occ_decompress(occ_mat P, occ_mat Q, occ_mat out, cudaStream_t stream
   return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_decompress launch");
 }
 
+}  // extern "C"
+
+// ------------------------------------------------------------------ occ_dplink (f1, DP)
+// Mailbox of one rank: two slots of D sub-slots of cap fp32 (sub-slot q is
+// written by member q), then the words: +4 q flag from member q (its sub-slot
+// of sequence seq is complete), +64 + 4 q ack from member q (q has summed its
+// slot of sequence seq, so ours may be rewritten), +1024 / +1088 the local
+// CTA-exit counters.  Every rank maps every member's mailbox with CUDA IPC.
+struct occ_dplink_s {
+  occ_comm dp = nullptr;
+  int D = 1, rank = 0;
+  size_t cap = 0, words_off = 0;
+  char* local = nullptr;
+  char* base[kDplinkMax] = {};
+  bool ipc[kDplinkMax] = {};
+  unsigned seq = 0;
+};
+
+static cudaError_t run_dplink_allreduce(occ_dplink L, const float* src, float* dst, size_t count, cudaStream_t st) {
+  DplinkArgs a{};
+  a.D = L->D;
+  a.rank = L->rank;
+  a.seq = ++L->seq;
+  a.cap = (long long)L->cap;
+  a.words_off = (long long)L->words_off;
+  for (int q = 0; q < L->D; q++) a.base[q] = L->base[q];
+  a.src = src;
+  a.dst = dst;
+  a.count = (long long)count;
+  return run_dplink_kernel(a, st);
+}
+
+static occ_status allreduce_factors_impl(int nmat, const occ_mat* G, const occ_mat* err, const occ_mat* Q,
+                                         const occ_mat* P, const int* r, float scale, uint32_t flags, occ_comm dp,
+                                         occ_dplink dl, void* ws, size_t ws_bytes, cudaStream_t stream);
+
+extern "C" {
+
 occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err, const occ_mat* Q, const occ_mat* P,
                                  const int* r, float scale, uint32_t flags, occ_comm dp, void* ws, size_t ws_bytes,
                                  cudaStream_t stream) {
   NvtxRange nvtx_("occ_allreduce_factors");
+  return allreduce_factors_impl(nmat, G, err, Q, P, r, scale, flags, dp, nullptr, ws, ws_bytes, stream);
+}
+
+}  // extern "C"
+
+// The DP step (occ_allreduce_factors / occ_allreduce_factors_link): the factor
+// sums run over NCCL (dp) or in-kernel over NVLink peer memory (dl).
+static occ_status allreduce_factors_impl(int nmat, const occ_mat* G, const occ_mat* err, const occ_mat* Q,
+                                         const occ_mat* P, const int* r, float scale, uint32_t flags, occ_comm dp,
+                                         occ_dplink dl, void* ws, size_t ws_bytes, cudaStream_t stream) {
   if (nmat < 1 || !G || !Q || !P || !r) return fail(OCC_ERR_INVALID_ARG, "null array or nmat < 1");
   if (!(flags & OCC_NO_EF) && !err) return fail(OCC_ERR_INVALID_ARG, "err array required unless OCC_NO_EF");
   if (flags & OCC_WIRE_BF16) return fail(OCC_ERR_UNSUPPORTED, "OCC_WIRE_BF16 applies to the send / recv calls");
@@ -476,7 +524,17 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
   if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(OCC_ERR_ALIGN, "workspace not 256-byte aligned");
   const bool multi = want_multi(flags);
   const bool dpl = !(flags & OCC_EF_GLOBAL);
-  const bool comm = dp != nullptr;   // a 1-rank group still runs its NCCL calls (tested on 1 GPU)
+  const bool comm = dp != nullptr || dl != nullptr;   // a 1-rank group still runs its exchange (tested on 1 GPU)
+  // sum over the group: NCCL, or the in-kernel exchange over the dplink
+  auto allreduce = [&](const float* src, float* dst, size_t count, const char* what) -> occ_status {
+    if (dl) {
+      if (count > dl->cap) return fail(OCC_ERR_WORKSPACE, "%s: %zu floats > dplink capacity %zu", what, count, dl->cap);
+      cudaError_t e = run_dplink_allreduce(dl, src, dst, count, stream);
+      return e == cudaSuccess ? OCC_OK : cuda_fail(e, what);
+    }
+    ncclResult_t nr = ncclAllReduce(src, dst, count, ncclFloat, ncclSum, dp->comm, stream);
+    return nr == ncclSuccess ? OCC_OK : nccl_fail(nr, what);
+  };
   char* base = static_cast<char*>(ws);
   float* pb = reinterpret_cast<float*>(base + L.p_bucket);
   float* qwb = reinterpret_cast<float*>(base + L.qw_bucket);
@@ -508,8 +566,7 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
       if (e != cudaSuccess) return cuda_fail(e, "dp (ORIENT_T) sweep launch");
     }
     if (comm) {
-      ncclResult_t nr = ncclAllReduce(qwb, qwb, qtot, ncclFloat, ncclSum, dp->comm, stream);
-      if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(U)");
+      if (occ_status sa = allreduce(qwb, qwb, qtot, "allreduce(U)")) return sa;
     }
     for (int i = 0; i < nmat; i++) {
       auto [p, g] = params_for(i);
@@ -525,8 +582,7 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
     }
     float* vsum = pb;
     if (comm) {
-      ncclResult_t nr = ncclAllReduce(pb, qsb, ptot, ncclFloat, ncclSum, dp->comm, stream);
-      if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(V)");
+      if (occ_status sa = allreduce(pb, qsb, ptot, "allreduce(V)")) return sa;
       vsum = qsb;
     }
     for (int i = 0; i < nmat; i++) {
@@ -554,8 +610,7 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
   }
   // (a3) allreduce-sum P over the DP group (reading C1)
   if (comm) {
-    ncclResult_t nr = ncclAllReduce(pb, pb, ptot, ncclFloat, ncclSum, dp->comm, stream);
-    if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(P)");
+    if (occ_status sa = allreduce(pb, pb, ptot, "allreduce(P)")) return sa;
   }
   // (a4-a5) Gram + orthonormalise + sweep 2 + Q reduce into the Q_w bucket
   for (int i = 0; i < nmat; i++) {
@@ -569,8 +624,7 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
   // (a6) allreduce-sum Q
   float* qsum = qwb;
   if (comm) {
-    ncclResult_t nr = ncclAllReduce(qwb, qsb, qtot, ncclFloat, ncclSum, dp->comm, stream);
-    if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllReduce(Q)");
+    if (occ_status sa = allreduce(qwb, qsb, qtot, "allreduce(Q)")) return sa;
     qsum = qsb;
   }
   // (a7-a9) M' = round(P_hat (scale sum Q)^T) over G, residual, warm start
@@ -589,6 +643,8 @@ occ_status occ_allreduce_factors(int nmat, const occ_mat* G, const occ_mat* err,
   }
   return OCC_OK;
 }
+
+extern "C" {
 
 occ_status occ_send_factors(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, int peer, uint32_t flags,
                             occ_comm pp, void* ws, size_t ws_bytes, cudaStream_t stream) {
@@ -945,6 +1001,91 @@ extern "C" occ_status occ_link_close(occ_link L) {
   cudaFree(L->local);
   delete L;
   return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_link_close");
+}
+
+extern "C" occ_status occ_dplink_open(occ_comm dp, int64_t max_floats, occ_dplink* out) {
+  NvtxRange nvtx_("occ_dplink_open");
+  if (!dp || !out) return fail(OCC_ERR_INVALID_ARG, "null communicator or output");
+  if (dp->nranks > kDplinkMax) return fail(OCC_ERR_UNSUPPORTED, "dplink: at most %d ranks", kDplinkMax);
+  if (max_floats < 1) return fail(OCC_ERR_SHAPE, "bad dplink capacity");
+  occ_dplink L = new occ_dplink_s;
+  L->dp = dp;
+  L->D = dp->nranks;
+  L->rank = dp->rank;
+  L->cap = ((size_t)max_floats + 63) / 64 * 64;
+  L->words_off = 2 * (size_t)L->D * L->cap * 4;
+  const size_t bytes = L->words_off + 2048;
+  auto bail = [&](occ_status st) {
+    for (int q = 0; q < L->D; q++)
+      if (L->ipc[q]) cudaIpcCloseMemHandle(L->base[q]);
+    if (L->local) cudaFree(L->local);
+    delete L;
+    return st;
+  };
+  cudaError_t e = cudaMalloc(&L->local, bytes);
+  if (e == cudaSuccess) e = cudaMemset(L->local, 0, bytes);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "dplink mailbox"));
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, L->local);
+  if (e != cudaSuccess) return bail(cuda_fail(e, "cudaIpcGetMemHandle"));
+  const int n = L->D;
+  char* dbuf = nullptr;
+  e = cudaMalloc(&dbuf, (size_t)(n + 1) * sizeof h);
+  if (e == cudaSuccess) e = cudaMemcpy(dbuf + (size_t)n * sizeof h, &h, sizeof h, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (dbuf) cudaFree(dbuf);
+    return bail(cuda_fail(e, "dplink handle exchange"));
+  }
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  ncclResult_t nr = ncclAllGather(dbuf + (size_t)n * sizeof h, dbuf, sizeof h, ncclUint8, dp->comm, st);
+  e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  std::string hb((size_t)n * sizeof h, '\0');
+  if (nr == ncclSuccess && e == cudaSuccess) e = cudaMemcpy(&hb[0], dbuf, hb.size(), cudaMemcpyDeviceToHost);
+  cudaFree(dbuf);
+  if (nr != ncclSuccess) return bail(nccl_fail(nr, "ncclAllGather(dplink handles)"));
+  if (e != cudaSuccess) return bail(cuda_fail(e, "dplink handle exchange"));
+  for (int q = 0; q < n; q++) {
+    if (q == L->rank) { L->base[q] = L->local; continue; }
+    cudaIpcMemHandle_t ph;
+    memcpy(&ph, hb.data() + (size_t)q * sizeof ph, sizeof ph);
+    cudaError_t e2 = cudaIpcOpenMemHandle(reinterpret_cast<void**>(&L->base[q]), ph, cudaIpcMemLazyEnablePeerAccess);
+    if (e2 != cudaSuccess) return bail(cuda_fail(e2, "cudaIpcOpenMemHandle (dplink)"));
+    L->ipc[q] = true;
+  }
+  *out = L;
+  return OCC_OK;
+}
+
+extern "C" occ_status occ_dplink_close(occ_dplink L) {
+  if (!L) return OCC_OK;
+  cudaError_t e = cudaDeviceSynchronize();
+  for (int q = 0; q < L->D; q++)
+    if (L->ipc[q]) cudaIpcCloseMemHandle(L->base[q]);
+  cudaFree(L->local);
+  delete L;
+  return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_dplink_close");
+}
+
+extern "C" occ_status occ_dplink_allreduce(occ_dplink link, const float* src, float* dst, int64_t count,
+                                           cudaStream_t stream) {
+  NvtxRange nvtx_("occ_dplink_allreduce");
+  if (!link || !src || !dst) return fail(OCC_ERR_INVALID_ARG, "null dplink or buffer");
+  if (count < 0 || (size_t)count > link->cap) return fail(OCC_ERR_WORKSPACE, "count %lld outside the dplink capacity %zu",
+                                                         (long long)count, link->cap);
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return fail(OCC_ERR_ALIGN, "src / dst not 16-byte aligned");
+  const cudaError_t e = run_dplink_allreduce(link, src, dst, (size_t)count, stream);
+  return e == cudaSuccess ? OCC_OK : cuda_fail(e, "occ_dplink_allreduce");
+}
+
+extern "C" occ_status occ_allreduce_factors_link(int nmat, const occ_mat* G, const occ_mat* err, const occ_mat* Q,
+                                                 const occ_mat* P, const int* r, float scale, uint32_t flags,
+                                                 occ_dplink link, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  NvtxRange nvtx_("occ_allreduce_factors_link");
+  if (!link) return fail(OCC_ERR_INVALID_ARG, "null dplink");
+  return allreduce_factors_impl(nmat, G, err, Q, P, r, scale, flags, nullptr, link, ws, ws_bytes, stream);
 }
 
 extern "C" occ_status occ_sendrecv_factors_link(occ_mat M, occ_mat err, occ_mat Q, occ_mat P, int r, occ_mat out,

@@ -85,6 +85,18 @@ cudaError_t run_link_exchange(const float* sP, const float* sQ, float* pP, float
                               const unsigned* flag_in, unsigned* recv_ctr, unsigned* peer_ack, unsigned rseq,
                               cudaStream_t st);
 unsigned take_link_timeout();
+// occ_dplink: the in-kernel allreduce-sum of a DP group over NVLink peer memory (occ_v2.cu)
+constexpr int kDplinkMax = 8;
+struct DplinkArgs {
+  int D, rank;
+  unsigned seq;
+  long long cap, words_off;   // floats per slot; byte offset of the words
+  char* base[kDplinkMax];     // every member's mailbox (this rank's own included)
+  const float* src;
+  float* dst;
+  long long count;
+};
+cudaError_t run_dplink_kernel(const DplinkArgs& a, cudaStream_t st);
 // tcgen05 sweeps (occ_umma.cu): workspace of the split, transposed small factor
 size_t umma_qt_bytes(int64_t n, int64_t m, int r);
 bool umma_applies(const Params& p, int r);

@@ -732,6 +732,94 @@ cudaError_t run_link_exchange(const float* sP, const float* sQ, float* pP, float
   return cudaGetLastError();
 }
 
+// occ_dplink allreduce-sum (occ_api.cu), push protocol (as occ_link: NVLink
+// stores into the peer's memory, every read local): a rank writes its bucket
+// into sub-slot [rank] of slot seq % 2 of every OTHER member's mailbox, and
+// once every CTA has written, releases flag[rank] = seq in each of them
+// (system scope); it then acquires its own flags[q] >= seq for every other q,
+// sums the D terms in rank order (its own from src; bit-identical on every
+// rank) into dst,
+// and the last CTA acknowledges ack[rank] = seq in every member's mailbox.  A
+// slot is rewritten two calls later, after every member's acknowledgement.
+// Words (unsigned): flag[q] at 0 + q, ack[q] at 16 + q, CTA counters at 256, 272.
+__global__ void __launch_bounds__(256) occ_dplink_kernel(const __grid_constant__ DplinkArgs a) {
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x, gs = (long long)gridDim.x * blockDim.x;
+  const int slot = (int)(a.seq & 1u);
+  auto words = [&](int q) { return reinterpret_cast<unsigned*>(a.base[q] + a.words_off); };
+  auto sub = [&](int q, int from) {   // member q's mailbox: sub-slot [from] of this call's slot
+    return reinterpret_cast<float*>(a.base[q]) + ((size_t)slot * a.D + from) * a.cap;
+  };
+  unsigned* mine = words(a.rank);
+  if (threadIdx.x == 0 && a.seq > 2)
+    for (int q = 0; q < a.D; q++)
+      if (q != a.rank) link_wait_geq(mine + 16 + q, a.seq - 2);   // every member is done with seq - 2
+  __syncthreads();
+  const long long nv = a.count / 4;
+  for (int q0 = 1; q0 < a.D; q0++) {   // the own term is read from src in the sum
+    const int q = (a.rank + q0) % a.D;   // spread the pushes over the members
+    float* d = sub(q, a.rank);
+    for (long long x = gt; x < nv; x += gs)
+      reinterpret_cast<float4*>(d)[x] = __ldcg(reinterpret_cast<const float4*>(a.src) + x);
+    for (long long x = 4 * nv + gt; x < a.count; x += gs) d[x] = __ldcg(a.src + x);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned old = atomicAdd(mine + 256, 1u);
+    if (old == gridDim.x - 1) {   // the last CTA out of the pushes releases flag[rank] everywhere
+      atomicExch(mine + 256, 0u);
+      __threadfence_system();
+      for (int q = 0; q < a.D; q++) link_release(words(q) + a.rank, a.seq);
+    }
+    for (int q = 0; q < a.D; q++)
+      if (q != a.rank) link_wait_geq(mine + q, a.seq);
+  }
+  __syncthreads();
+  // the sum in rank order; the own term straight from src (dst may alias src:
+  // each element is read before it is written, by the same thread)
+  auto term4 = [&](int q, long long x) {
+    return __ldcg(reinterpret_cast<const float4*>(q == a.rank ? a.src : sub(a.rank, q)) + x);
+  };
+  for (long long x = gt; x < nv; x += gs) {
+    float4 v = term4(0, x);
+    for (int q = 1; q < a.D; q++) {
+      const float4 w = term4(q, x);
+      v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+    }
+    reinterpret_cast<float4*>(a.dst)[x] = v;
+  }
+  for (long long x = 4 * nv + gt; x < a.count; x += gs) {
+    float v = __ldcg((0 == a.rank ? a.src : sub(a.rank, 0)) + x);
+    for (int q = 1; q < a.D; q++) v += __ldcg((q == a.rank ? a.src : sub(a.rank, q)) + x);
+    a.dst[x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {   // the last CTA out acknowledges seq to every member
+    __threadfence_system();
+    const unsigned old = atomicAdd(mine + 272, 1u);
+    if (old == gridDim.x - 1) {
+      atomicExch(mine + 272, 0u);
+      __threadfence_system();
+      for (int q = 0; q < a.D; q++)
+        if (q != a.rank) link_release(words(q) + 16 + a.rank, a.seq);
+    }
+  }
+}
+
+cudaError_t run_dplink_kernel(const DplinkArgs& a, cudaStream_t st) {
+  // enough CTAs to stream the peers' slots at NVLink speed; every CTA pays a
+  // system-scope fence, and all must be co-resident (they wait on each other
+  // only through the flag, which the LAST copying CTA releases)
+  static const int cap = [] {   // OCC_DPLINK_GRID: CTA cap (experiment), default 148
+    const char* e = getenv("OCC_DPLINK_GRID");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? std::min(v, 148) : 148;
+  }();
+  const int grid = (int)std::max<long long>(1, std::min<long long>(cap, (a.count / 4 + 2047) / 2048));
+  occ_dplink_kernel<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 unsigned take_link_timeout() {
   unsigned v = 0, z = 0;
   if (cudaMemcpyFromSymbol(&v, g_link_timeout, sizeof v) != cudaSuccess) return 0;

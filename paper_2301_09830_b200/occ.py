@@ -79,6 +79,12 @@ def lib():
         "occ_link_open": ([vp, c_int, c_int, i64, i64, c_int, ctypes.POINTER(vp)], c_int),
         "occ_link_close": ([vp], c_int),
         "occ_sendrecv_factors_link": ([M, M, M, M, c_int, M, M, M, u32, vp, vp, ctypes.c_size_t, vp], c_int),
+        "occ_dplink_open": ([vp, i64, ctypes.POINTER(vp)], c_int),
+        "occ_dplink_close": ([vp], c_int),
+        "occ_dplink_allreduce": ([vp, vp, vp, i64, vp], c_int),
+        "occ_allreduce_factors_link": ([c_int, ctypes.POINTER(M), ctypes.POINTER(M), ctypes.POINTER(M),
+                                        ctypes.POINTER(M), ctypes.POINTER(c_int), ctypes.c_float, u32, vp, vp,
+                                        ctypes.c_size_t, vp], c_int),
         "occ_get_unique_id": ([ctypes.c_char_p], c_int),
         "occ_comm_init": ([ctypes.POINTER(vp), ctypes.c_char_p, c_int, c_int], c_int),
         "occ_comm_split": ([vp, c_int, c_int, ctypes.POINTER(vp)], c_int),
@@ -177,6 +183,23 @@ def occ_allreduce_factors(G: Sequence, err: Optional[Sequence], Q: Sequence, P: 
                              device=G[0].device)
     _check(lib().occ_allreduce_factors(n, g_, e_, q_, p_, rs, scale, flags, comm.handle if comm else None,
                                        ws.data_ptr(), ws.numel(), _stream(stream)), "occ_allreduce_factors")
+    return ws
+
+
+def occ_allreduce_factors_link(G: Sequence, err: Optional[Sequence], Q: Sequence, P: Sequence, r: int,
+                               scale: float, link: "DpLink", flags: int = 0, ws=None, stream=None):
+    """occ_allreduce_factors with the two factor sums done in-kernel over the
+    DP group's NVLink mailboxes (include/occ.h occ_dplink)."""
+    n = len(G)
+    arr = occ_mat * n
+    g_, q_, p_ = arr(*[mat(x) for x in G]), arr(*[mat(x) for x in Q]), arr(*[mat(x) for x in P])
+    e_ = arr(*[mat(x) for x in err]) if err is not None else None
+    rs = (ctypes.c_int * n)(*([r] * n))
+    if ws is None:
+        ws = alloc_workspace(max(x.shape[0] for x in G), max(x.shape[1] for x in G), r, nmat=n,
+                             device=G[0].device)
+    _check(lib().occ_allreduce_factors_link(n, g_, e_, q_, p_, rs, scale, flags, link.handle, ws.data_ptr(),
+                                            ws.numel(), _stream(stream)), "occ_allreduce_factors_link")
     return ws
 
 
@@ -315,4 +338,28 @@ class Link:
     def close(self):
         if self.handle:
             _check(lib().occ_link_close(self.handle), "occ_link_close")
+            self.handle = None
+
+
+class DpLink:
+    """An occ_dplink: the DP group's NVLink mailboxes for the in-kernel factor
+    sums (include/occ.h).  open() is collective over the communicator."""
+
+    def __init__(self, handle: int):
+        self.handle = ctypes.c_void_p(handle)
+
+    @classmethod
+    def open(cls, comm: "Comm", max_floats: int) -> "DpLink":
+        h = ctypes.c_void_p()
+        _check(lib().occ_dplink_open(comm.handle, max_floats, ctypes.byref(h)), "occ_dplink_open")
+        return cls(h.value)
+
+    def allreduce(self, src, dst, stream=None):
+        """dst = sum over the group of src (fp32 device tensors), in rank order."""
+        _check(lib().occ_dplink_allreduce(self.handle, src.data_ptr(), dst.data_ptr(), src.numel(), _stream(stream)),
+               "occ_dplink_allreduce")
+
+    def close(self):
+        if self.handle:
+            _check(lib().occ_dplink_close(self.handle), "occ_dplink_close")
             self.handle = None

@@ -101,6 +101,48 @@ def main():
         report(name, recon_rel=e_recon, err_rel=e_err, q_rel=q_rel, orth=orth, identical_on_ranks=same,
                ok=e_recon <= 1e-4 and e_err <= 1e-4 and same and orth <= 1e-5 and q_rel <= 1e-3)
 
+    # ------------------------------------------------------------------ DP over the in-kernel exchange (occ_dplink, f1)
+    dl = occ.DpLink.open(comm, (12288 + 9216) * 64)
+    for flags, name, (n, m, r) in ((0, "dp_link_local_ef", (768, 1024, 16)),
+                                   (occ.OCC_EF_GLOBAL, "dp_link_global_ef", (768, 1024, 16)),
+                                   (occ.OCC_ORIENT_T, "dp_link_orient_t", (1536, 512, 16)),
+                                   (0, "dp_link_c4_mlp_r64", (3072, 12288, 64))):
+        ot = bool(flags & occ.OCC_ORIENT_T)
+        Ms = [synth.d2_gradlike(n, m, 540 + w) for w in range(world)]
+        Es = [synth.e0(n, m, 640 + w, like=Ms[w]) for w in range(world)]
+        Q0 = synth.q0(n if ot else m, r, 17)
+        G = torch.from_numpy(Ms[rank]).to(dev)
+        E = torch.from_numpy(Es[rank]).to(dev)
+        Q = torch.from_numpy(Q0).to(dev)
+        P = torch.empty(m if ot else n, r, device=dev)
+        occ.occ_allreduce_factors_link([G], [E], [Q], [P], r, 1.0 / world, dl, flags=flags)
+        occ.occ_check_status(comm=comm)
+        o = oracle.dp_step(Ms, Es, Q0, scale=1.0 / world, ef_global=bool(flags & occ.OCC_EF_GLOBAL), orient_t=ot)
+        A = sum(Ms[w].astype(np.float64) + Es[w] for w in range(world))
+        gs, es = gather_np(G), gather_np(E)
+        e_recon = max(rel(gs[w], o["recon"], A / world) for w in range(world))
+        e_err = max(rel(es[w], o["err"][w], Ms[w].astype(np.float64) + Es[w]) for w in range(world))
+        same = all(np.array_equal(gs[0], gs[w]) for w in range(world))
+        Ph = P.double().cpu().numpy()
+        orth = float(np.linalg.norm(Ph.T @ Ph - np.eye(r)))
+        q_rel = rel(Q.double().cpu().numpy(), o["Q"], o["Q"])
+        report(name, recon_rel=e_recon, err_rel=e_err, q_rel=q_rel, orth=orth, identical_on_ranks=same,
+               ok=e_recon <= 1e-4 and e_err <= 1e-4 and same and orth <= 1e-5 and q_rel <= 1e-3)
+    # slot reuse: 6 back-to-back calls (each slot three times), every rank identical
+    n, m, r = 512, 768, 16
+    G = torch.from_numpy(synth.d2_gradlike(n, m, 560 + rank)).to(dev)
+    E = torch.zeros(n, m, device=dev)
+    Q = torch.from_numpy(synth.q0(m, r, 19)).to(dev)
+    P = torch.empty(n, r, device=dev)
+    for _ in range(6):
+        occ.occ_allreduce_factors_link([G], [E], [Q], [P], r, 1.0 / world, dl)
+    occ.occ_check_status(comm=comm)
+    qs = gather_np(Q)
+    report("dp_link_slot_reuse", calls=6, identical_on_ranks=all(np.array_equal(qs[0], x) for x in qs),
+           finite=bool(torch.isfinite(Q).all()),
+           ok=all(np.array_equal(qs[0], x) for x in qs) and bool(torch.isfinite(Q).all()))
+    dl.close()
+
     # PP checks run twice: fp32 factors, and OCC_WIRE_BF16 (reading C7: bf16 factors on
     # the wire, e_new against them; the oracle rounds its fp64 factors the same way,
     # so a few elements may differ by one bf16 ulp -> 1e-3)

@@ -198,3 +198,20 @@ def test_link_argument_errors(L):
     s = L.occ_sendrecv_factors_link(M, E, Q, P, 16, M, P, Q, 0, None, ctypes.c_void_p(FAKE), 1 << 30, None)
     assert status_name(L, s) == "OCC_ERR_INVALID_ARG"
     assert {"occ_link_open", "occ_link_close", "occ_sendrecv_factors_link"} <= set(declared_functions())
+
+
+def test_dplink_argument_errors(L):
+    """occ_dplink (f1, DP): null handles are rejected on the host."""
+    h = ctypes.c_void_p()
+    assert status_name(L, L.occ_dplink_open(None, 1024, ctypes.byref(h))) == "OCC_ERR_INVALID_ARG"
+    assert L.occ_dplink_close(None) == 0
+    M, E, Q, P = good()
+    arr = occ.occ_mat * 1
+    rs = (ctypes.c_int * 1)(16)
+    s = L.occ_allreduce_factors_link(1, arr(M), arr(E), arr(Q), arr(P), rs, ctypes.c_float(1.0), 0, None,
+                                     ctypes.c_void_p(FAKE), 1 << 30, None)
+    assert status_name(L, s) == "OCC_ERR_INVALID_ARG"
+    assert status_name(L, L.occ_dplink_allreduce(None, ctypes.c_void_p(FAKE), ctypes.c_void_p(FAKE), 16, None)) == \
+        "OCC_ERR_INVALID_ARG"
+    assert {"occ_dplink_open", "occ_dplink_close", "occ_dplink_allreduce",
+            "occ_allreduce_factors_link"} <= set(declared_functions())

@@ -524,6 +524,54 @@ def test_single_rank_nccl_allreduce_factors():
         comm.destroy()
 
 
+@pytest.mark.parametrize("r,flags", [(64, 0), (32, "EF_GLOBAL"), (64, "ORIENT_T")])
+def test_dplink_single_rank_matches_oracle(r, flags):
+    """occ_allreduce_factors_link on a 1-rank group: the in-kernel exchange runs
+    (push into the own mailbox, flag, sum, acknowledge; 5 calls so both slots
+    are reused), the result matches the oracle's dp_step and, bit for bit, the
+    NCCL call on the same communicator."""
+    fl = {0: 0, "EF_GLOBAL": occ.OCC_EF_GLOBAL, "ORIENT_T": occ.OCC_ORIENT_T}[flags]
+    shapes = [(640, 1024), (512, 776)]
+    Ms = [synth.d2_gradlike(n, m, 141 + j) for j, (n, m) in enumerate(shapes)]
+    es = [synth.e0(n, m, 151 + j, like=Ms[j]) for j, (n, m) in enumerate(shapes)]
+    ot = fl & occ.OCC_ORIENT_T
+    Q0s = [synth.q0(n if ot else m, r, 161 + j) for j, (n, m) in enumerate(shapes)]
+    comm = occ.Comm.single()
+    link = occ.DpLink.open(comm, max(sum(max(n, m) for n, m in shapes) * r, 1))
+    try:
+        res = {}
+        for mode in ("link", "nccl"):
+            G = [to_dev(x) for x in Ms]
+            E = [to_dev(x) for x in es]
+            Q = [to_dev(x) for x in Q0s]
+            P = [torch.empty(m if ot else n, r, device="cuda") for n, m in shapes]
+            for it in range(5):
+                if it:   # fresh gradients each call, warm start and error carried
+                    for j in range(len(shapes)):
+                        G[j].copy_(to_dev(Ms[j]))
+                if mode == "link":
+                    occ.occ_allreduce_factors_link(G, E, Q, P, r, 1.0, link, flags=fl)
+                else:
+                    occ.occ_allreduce_factors(G, E, Q, P, r, 1.0, flags=fl, comm=comm)
+                occ.occ_check_status(comm=comm)
+                if it == 0:
+                    res[mode + "0"] = [x.clone() for x in G] + [x.clone() for x in E]
+            res[mode] = G + E + Q + P
+        for a, b in zip(res["link"], res["nccl"]):
+            assert torch.equal(a, b)
+        for j in range(len(shapes)):   # each matrix of the bucket: a 1-rank dp_step
+            o = oracle.dp_step([Ms[j]], [es[j]], Q0s[j], scale=1.0, ef_global=bool(fl & occ.OCC_EF_GLOBAL),
+                               orient_t=bool(ot))
+            A = Ms[j].astype(np.float64) + es[j]
+            Gj = res["link0"][j].double().cpu().numpy()
+            Ej = res["link0"][len(shapes) + j].double().cpu().numpy()
+            assert rel(Gj, o["recon"], A) <= TOL32 and elem(Gj, o["recon"], A) <= TOL32 / 10
+            assert rel(Ej, o["err"][0], A) <= TOL32
+    finally:
+        link.close()
+        comm.destroy()
+
+
 @pytest.mark.parametrize("wire", [False, True])
 def test_single_rank_nccl_sendrecv_self(wire):
     """occ_sendrecv_factors on a 1-rank communicator, the stage its own peer:
