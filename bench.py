@@ -220,6 +220,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-target", action="store_true", help="skip the north-star T line (C2 only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N = 1: time the back-to-back steps eagerly only (default: CUDA-graph replay, eager beside it)")
     ap.add_argument("--exchange", default="link", choices=["link", "nccl"],
                     help="N > 1 pipeline ring: in-kernel NVLink exchange (occ_link, default) or NCCL send/recv")
     args = ap.parse_args()
@@ -335,17 +337,48 @@ def main():
         for k in range(warmup):
             sets[k % nsets]()
         barrier()
-        # (1) back to back over the rotating sets: the headline per-step time
-        sampler = ClockSampler(local)
-        with sampler:
+        # (1) back to back over the rotating sets: the headline per-step time.  At
+        # N = 1 the steps' API calls are captured once per rotation into a CUDA
+        # graph and replayed (the same kernels with the same arguments: outputs
+        # bit-identical, tools/graph_probe.py); the eager loop is timed beside it.
+        # N > 1 stays eager (the link protocols number their calls on the host).
+        graph = None
+        if world == 1 and not args.no_graph:
+            try:
+                cs = torch.cuda.Stream(device=dev)
+                cs.wait_stream(torch.cuda.current_stream())
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=cs):
+                    for k in range(nsets):
+                        sets[k]()
+                torch.cuda.synchronize()
+                graph.replay()
+                torch.cuda.synchronize()
+            except Exception as exc:   # noqa: BLE001
+                print(f"bench: graph capture unavailable ({exc}); eager only", file=sys.stderr)
+                graph = None
+
+        def timed_loop(use_graph):
             barrier()
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0.record(stream)
-            for k in range(steps):
-                sets[k % nsets]()
+            if use_graph:
+                for _ in range(steps // nsets):
+                    graph.replay()
+                for k in range(steps % nsets):
+                    sets[k]()
+            else:
+                for k in range(steps):
+                    sets[k % nsets]()
             t1.record(stream)
             barrier()
-        ms = max_over_ranks(t0.elapsed_time(t1) / steps)
+            return max_over_ranks(t0.elapsed_time(t1) / steps)
+
+        sampler = ClockSampler(local)
+        with sampler:
+            eager_ms = timed_loop(False)
+            ms = timed_loop(True) if graph is not None else eager_ms
         # (2) each step alone after a 2x-L2 write flush, events around it
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         barrier()
@@ -359,7 +392,8 @@ def main():
         per = {"median_ms": max_over_ranks(float(np.median(t))), "p10_ms": max_over_ranks(float(np.percentile(t, 10))),
                "p90_ms": max_over_ranks(float(np.percentile(t, 90))), "mean_ms": max_over_ranks(float(t.mean()))}
         stats = occ.occ_read_stats(sets[0].ws)
-        return {"ms": ms, "per_step": per, "clocks": sampler.summary(), "stats": stats, "sets": sets, "nsets": nsets}
+        return {"ms": ms, "eager_ms": eager_ms, "graph": graph is not None, "per_step": per,
+                "clocks": sampler.summary(), "stats": stats, "sets": sets, "nsets": nsets}
 
     def count_launches(step):
         """Kernels of OURS launched by one step (torch profiler, untimed)."""
@@ -550,7 +584,8 @@ def main():
     if name == "C2" and world == 1 and not args.no_target:
         t = bench_config("T", args.steps, args.warmup)
         tab = alg_bytes(CONFIGS["T"], 1)
-        target = {"workload": CONFIGS["T"]["desc"], "ms_per_step": t["ms"], "per_step_flushed": t["per_step"],
+        target = {"workload": CONFIGS["T"]["desc"], "ms_per_step": t["ms"], "eager_ms_per_step": t["eager_ms"],
+                  "per_step_flushed": t["per_step"],
                   "value": 1024 * 3072 * 4 / (t["ms"] * 1e-3) / 1e9, "unit": "GB/s",
                   "roofline_frac": tab / (t["ms"] * 1e-3) / 1e9 / hbm_peak,
                   "roofline_frac_flushed_median": tab / (t["per_step"]["median_ms"] * 1e-3) / 1e9 / hbm_peak}
@@ -584,11 +619,15 @@ def main():
         cd = config_dict(name, world, parallelism)
         cd["l2"] = (f"inputs larger than L2: {res['nsets']} rotating input sets of {elems(cfg) * 12 / 1e6:.0f} MB "
                     f"(M, e, M') back to back; per_step: each step alone after a 2x-L2 write flush")
+        cd["timing"] = ("back to back: one rotation of the steps' API calls captured in a CUDA graph and replayed "
+                        "(eager_ms_per_step: the same loop issued eagerly)" if res["graph"] else
+                        "back to back, eager")
         cd["path"] = {1: "v1 fused persistent kernel", 2: "per-phase launches",
                       3: "fused TMEM-resident persistent kernel"}.get(res["stats"]["path"], "per-phase launches")
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "eager_ms_per_step": res["eager_ms"],
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, DESIGN.md §4 D2 gradient-like)",
             "config": cd,
             "per_step_flushed": res["per_step"],

@@ -742,3 +742,36 @@ def test_dp_mixed_shape_bucket_matches_oracle():
         G = Gd[i].double().cpu().numpy()
         assert rel(G, o["recon"], A) <= TOL32 and elem(G, o["recon"], A) <= TOL32 / 10, i
         assert rel(Ed[i].double().cpu().numpy(), o["err"][0], A) <= TOL32, i
+
+
+@pytest.mark.parametrize("n,m,r", [(1024, 3072, 16), (1000, 776, 64)])
+def test_graph_replay_matches_eager(n, m, r):
+    """bench.py times N = 1 steps as CUDA-graph replays of the same API calls:
+    a replayed step (fused kernel, r16; per-phase tcgen05 path, r64) is bit-identical
+    to the eagerly issued one, and both match the oracle."""
+    M = synth.d2_gradlike(n, m, 171)
+    e = synth.e0(n, m, 172, like=M)
+    Q0 = synth.q0(m, r, 173)
+    Md = to_dev(M)
+    ws = occ.alloc_workspace(n, m, r)
+    outs = {}
+    for mode in ("eager", "graph"):
+        Ed, Qd = to_dev(e), to_dev(Q0)
+        Pd = torch.empty(n, r, device="cuda")
+        Rd = torch.empty_like(Md)
+        if mode == "eager":
+            occ.occ_compress(Md, Ed, Qd, Pd, Rd, r=r, ws=ws)
+        else:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                occ.occ_compress(Md, Ed, Qd, Pd, Rd, r=r, ws=ws)
+            Ed.copy_(to_dev(e))
+            Qd.copy_(to_dev(Q0))
+            g.replay()
+        torch.cuda.synchronize()
+        outs[mode] = (Rd, Ed, Qd, Pd)
+    for a, b in zip(outs["eager"], outs["graph"]):
+        assert torch.equal(a, b)
+    o = oracle.compress_step(M, e, Q0)
+    A = M.astype(np.float64) + e
+    assert rel(outs["graph"][0].double().cpu().numpy(), o["recon"], A) <= TOL32
