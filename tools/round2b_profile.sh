@@ -9,7 +9,7 @@
 #   gpurun --timeout 3000 -- 'bash tools/round2b_profile.sh'
 set -u
 mkdir -p gpurun_out
-o=gpurun_out/r2g
+o=gpurun_out/${PREFIX:-r2g}
 timeout 1200 python -m pytest tests -m gpu -q > ${o}_pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 ${o}_pytest_gpu.log
 timeout 600 python bench.py > ${o}_bench_n1.json 2> ${o}_bench_n1.err || { echo "bench failed"; tail -5 ${o}_bench_n1.err; }
 tail -1 ${o}_bench_n1.json | cut -c1-200
