@@ -546,6 +546,8 @@ static occ_status allreduce_factors_impl(int nmat, const occ_mat* G, const occ_m
     poff[i] = ptot; ptot += (size_t)G[i].rows * R;
     qoff[i] = qtot; qtot += (size_t)G[i].cols * R;
   }
+  if (dl && std::max(ptot, qtot) > dl->cap)   // before anything is enqueued (occ.h conventions)
+    return fail(OCC_ERR_WORKSPACE, "factor bucket of %zu floats > dplink capacity %zu", std::max(ptot, qtot), dl->cap);
   auto params_for = [&](int i) {
     occ_mat e = err ? err[i] : occ_mat{nullptr, 0, 0, 0, OCC_F32};
     Params p = base_params(G[i], e, Q[i], P[i], flags);
