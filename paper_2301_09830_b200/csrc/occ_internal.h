@@ -100,6 +100,9 @@ cudaError_t run_dplink_kernel(const DplinkArgs& a, cudaStream_t st);
 // tcgen05 sweeps (occ_umma.cu): workspace of the split, transposed small factor
 size_t umma_qt_bytes(int64_t n, int64_t m, int r);
 bool umma_applies(const Params& p, int r);
+// dst = sum of S partials of count floats, stride floats apart (fixed order)
+cudaError_t run_reduce_partials(const float* src, long long stride, int S, float* dst, long long count,
+                                cudaStream_t st);
 // sweep 1 (transposed = false: P_part) or sweep 2 (true: Q_part) on tcgen05
 cudaError_t run_umma_sweep(const Params& p, int r, bool transposed, int max_splits, int* G_out, cudaStream_t st);
 // the DP reconstruction (phase F with f_tc) on tcgen05, r in {32, 64}

@@ -152,7 +152,9 @@ __global__ void __launch_bounds__(NT, 1) occ_step_kernel(const __grid_constant__
   }
   // stamped by the launch that ends the step's v1 part: phase F, or phase E when
   // F runs in the v2 reconstruct kernel (occ_api.cu reconstruct)
-  if (blockIdx.x == 0 && threadIdx.x == 0 && ph0 <= P_F && P_E < ph1) {
+  // (P_D == ph1: the orthonormalisation launch before a tcgen05 sweep 2, whose
+  // Q reduce is a plain launch)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ph0 <= P_F && (P_E < ph1 || ph1 == P_D)) {
     p.stats->path = p.path;
     p.stats->grid = gridDim.x;
     p.stats->q_amp = -1.0;
@@ -194,6 +196,8 @@ cudaError_t run_t(Params p, const Geometry& g, int ph0, int ph1, bool multi, cud
       p.s1 = G;
       ph0 = P_B1;
       if (ph0 >= ph1) return cudaSuccess;
+      if (ph1 <= P_B2)   // the P reduce alone (the DP path): a plain launch
+        return run_reduce_partials(p.P_part, (long long)p.n * R, G, p.P, (long long)p.n * R, st);
     } else if (eu != cudaErrorNotSupported) {
       return eu;
     }
@@ -209,6 +213,11 @@ cudaError_t run_t(Params p, const Geometry& g, int ph0, int ph1, bool multi, cud
     if (eu == cudaSuccess) {
       p.s2 = G;
       ph0 = P_E;
+      if (ph0 >= ph1) return cudaSuccess;
+      // the Q reduce (phase E) as a plain launch
+      const cudaError_t er = run_reduce_partials(p.Q_part, (long long)p.m * R, G, p.Qloc, (long long)p.m * R, st);
+      if (er != cudaSuccess) return er;
+      ph0 = P_F;
       if (ph0 >= ph1) return cudaSuccess;
     } else if (eu != cudaErrorNotSupported) {
       return eu;

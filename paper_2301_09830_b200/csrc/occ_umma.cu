@@ -663,6 +663,32 @@ __global__ void occ_split_rows_kernel(const __grid_constant__ SplitJobs jobs) {
   }
 }
 
+// dst = sum of S partials (src + s * stride, s = 0 .. S-1, fixed order) of
+// `count` floats: the sweeps' P / Q reduce as a plain launch (16-byte vectors,
+// 4 partials per step in flight) instead of a cooperative step-kernel phase.
+__global__ void __launch_bounds__(256) occ_reduce_partials_kernel(const float* __restrict__ src, long long stride,
+                                                                  int S, float* __restrict__ dst, long long count) {
+  const long long nv = count / 4, sv = stride / 4;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < nv; x += (long long)gridDim.x * blockDim.x) {
+    float4 v = __ldcg(s4 + x);
+    int k = 1;
+    for (; k + 3 < S; k += 4) {
+      const float4 a = __ldcg(s4 + x + k * sv), b = __ldcg(s4 + x + (k + 1) * sv);
+      const float4 c = __ldcg(s4 + x + (k + 2) * sv), d = __ldcg(s4 + x + (k + 3) * sv);
+      v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+      v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
+      v.x += c.x; v.y += c.y; v.z += c.z; v.w += c.w;
+      v.x += d.x; v.y += d.y; v.z += d.z; v.w += d.w;
+    }
+    for (; k < S; k++) {
+      const float4 a = __ldcg(s4 + x + k * sv);
+      v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
+    }
+    reinterpret_cast<float4*>(dst)[x] = v;
+  }
+}
+
 // Q^T split into hi / lo (tf32 split as above), K-major for the B operand:
 // th[k][c] = hi(Q[c][k]), tl[k][c] = lo(Q[c][k]), row stride ldt.
 __global__ void occ_split_t_kernel(const float* __restrict__ Q, int m, int R, unsigned* th, unsigned* tl, int ldt) {
@@ -873,6 +899,15 @@ static cudaError_t launch_recon(const Params& p, cudaStream_t st) {
 // the DP reconstruction: up to two column and two row factors, hi / lo (4 r (n + m))
 size_t umma_qt_bytes(int64_t n, int64_t m, int r) {
   return (4 * (size_t)(n + m) + 64) * (size_t)r * 4;
+}
+
+// count and stride are multiples of 4 (R >= 4 columns of fp32)
+cudaError_t run_reduce_partials(const float* src, long long stride, int S, float* dst, long long count,
+                                cudaStream_t st) {
+  const long long nv = count / 4;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((nv + 255) / 256, 148 * 8));
+  umma::occ_reduce_partials_kernel<<<grid, 256, 0, st>>>(src, stride, S, dst, count);
+  return cudaGetLastError();
 }
 
 bool umma_applies(const Params& p, int r) {
