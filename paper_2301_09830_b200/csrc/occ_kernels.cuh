@@ -897,10 +897,12 @@ __device__ int factor_fast(const Params& p, const double* part, int npart, bool 
   constexpr int NP = npairs(R);
   constexpr int TK = (NT / R) < R ? (NT / R) : R;  // threads along k per row
   const double tau2 = p.tau * p.tau;
-  for (int q = threadIdx.x; q < NP; q += NT) {
-    int a = 0, rem = q;
-    while (rem >= R - a) { rem -= R - a; a++; }
-    const int b = a + rem;
+  // (a, b) from the flat index and the packed offset in closed form: the
+  // decode loop of the other reducers costs O(R) per entry, ~5 us at R = 64
+  for (int x = threadIdx.x; x < R * R; x += NT) {
+    const int a = x / R, b = x % R;
+    if (a > b) continue;
+    const int q = pidx(R, a, b);
     double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;   // fixed order per entry
     int u = 0;
     for (; u + 3 < npart; u += 4) {
