@@ -35,7 +35,7 @@ python tools/dp_driver.py 3 > /dev/null 2>&1 && {
       -o ${o}_sweep2_C4 python tools/dp_driver.py 3 > ${o}_ncu_s2.log 2>&1; echo "sweep2 rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:umma_recon --launch-skip 2 -c 1 \
       -o ${o}_recon_C4 python tools/dp_driver.py 3 > ${o}_ncu_rc.log 2>&1; echo "recon rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:occ_step_kernel --launch-skip 8 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:occ_step_kernel --launch-skip 2 -c 1 \
       -o ${o}_orth_C4 python tools/dp_driver.py 3 > ${o}_ncu_orth.log 2>&1; echo "orth rc=$?"
 }
 for rep in ${o}_*.ncu-rep; do
