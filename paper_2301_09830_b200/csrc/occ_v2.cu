@@ -623,8 +623,26 @@ static cudaError_t launch2(const Params& p1, const Plan2& pl, void* ws_tail, cud
     while (pl.total > seen && !cur.compare_exchange_weak(seen, pl.total)) {
     }
   }
-  void* args[] = {&p};
-  return cudaLaunchCooperativeKernel((const void*)kern, dim3(pl.nr * pl.nc), dim3(NT), args, pl.total, st);
+  // cooperative (the grid barriers need every CTA resident) and, unless
+  // OCC_V2_PDL=0, programmatic dependent launch: the next kernel in the stream
+  // may begin launching once every CTA has started phase 5
+  static const bool pdl = [] {
+    const char* e = getenv("OCC_V2_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.nr * pl.nc);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = pl.total;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 template <int R>

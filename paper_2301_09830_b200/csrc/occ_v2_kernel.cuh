@@ -73,6 +73,10 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const unsigned tbase = tmem_base_sh;
+  // programmatic dependent launch: everything above touched only shared and
+  // tensor memory; global memory (inputs, workspace barrier words) waits for
+  // the previous grid in the stream to complete (a no-op without PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // TMEM: warp w reaches lanes 32 (w % 4) ..; the warps sharing a lane quadrant split its 512 columns
   const unsigned taddr_w = tbase + ((unsigned)((w & 3) * 32) << 16) + (unsigned)((w >> 2) * (512 / (NW / 4)));
   // TMEM slot of a cell: column-group major, so one column group's cells are contiguous
@@ -446,6 +450,9 @@ __global__ void __launch_bounds__(NT, 1) occ_v2_kernel(const __grid_constant__ P
       tr(10);
       if (stamp) p.stats->t_ns[5] = gtimer();
 
+      // the next step's grid may start launching (its CTAs wait for this grid's
+      // completion in griddepcontrol.wait before touching global memory)
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       // ---------------------------------------------------------- phase 5 (compute warps)
       // The A operand Q (M = columns 2g | 2g+1, K = rank) of a column group is
       // used by exactly one lane: it is loaded straight from L2 (no staging, no
