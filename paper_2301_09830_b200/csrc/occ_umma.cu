@@ -1,31 +1,35 @@
-// occ_umma.cu -- 5th-generation tensor-core (tcgen05) sweep of the per-phase
-// path: sweep 1, P_part = (M + e) Q_prev (north_star a1, a2; PAPER.md:269-270,
-// the PowerSGD power iteration P = M Q), for the shapes the fused kernel does
-// not hold on chip (BASELINE configs[2], configs[3]: r = 32, 64).
+// occ_umma.cu -- the per-phase path's streaming kernels on the 5th-generation
+// tensor cores (tcgen05, TMEM, TMA tensor maps), for the shapes the fused
+// kernel does not hold on chip (BASELINE configs[2], configs[3], the G^T
+// embedding: r = 16 .. 64, fp32 M):
+//   umma_sweep_kernel<R, false>  sweep 1, P_part = (M + e) Q_prev        (a1, a2)
+//   umma_sweep_kernel<R, true>   sweep 2, Q_part = (M + e)^T P_hat       (a1, a5)
+//   occ_reduce_partials_kernel   P / Q = the sum of the sweeps' partials
+//   umma_recon_kernel<R, MODE>   the DP reconstruction, M' and e_new      (a7, a8)
+// (north_star steps; PAPER.md:269-270 the PowerSGD power iteration, 383-389
+// lazy error propagation, 676-677 the DP allreduce of P and Q.)
 //
-// One persistent CTA per SM, warp-specialised:
+// Sweeps: one persistent CTA per SM, warp-specialised:
 //   warp 0      TMA producer: 2-D tensor-map loads (cp.async.bulk.tensor, 128-B
-//               swizzle) of a 128-row x 32-column box of M and of e, and of the
-//               32-column slices of Q_prev^T split into hi / lo (the small
-//               factor, pre-split and transposed once per step by
-//               occ_split_t_kernel), into an mbarrier ring of stages.
+//               swizzle) of a 128-row x 32-column box of M and of e (sweep 2:
+//               four 32 x 32 boxes, 128-B swizzle with 32-B atoms), and of the
+//               32-wide slices of the small factor's transpose split into hi / lo
+//               (pre-split once per step by occ_split_t_kernel), into an
+//               mbarrier ring of stages.
 //   warps 2..5  converters: A = M + e and the 3-term TF32 split A = A_hi + A_lo
 //               (hi: the low 13 mantissa bits masked off, lo = A - hi exact in
 //               fp32), in place (A_hi over the M box, A_lo over the e box) --
 //               elementwise, so the swizzled layout TMA wrote is kept as is.
-//   warp 1      MMA issuer (one thread): per stage and per 8-column K step,
-//               tcgen05.mma.kind::tf32 A_lo.Q_hi + A_hi.Q_lo + A_hi.Q_hi
-//               (fp32-level accuracy, as the mma.sync sweeps) into a 128 x R
-//               fp32 accumulator in TENSOR MEMORY; tcgen05.commit frees the
-//               stage back to the producer.
-//   epilogue    the converter warps read the accumulator (tcgen05.ld, lane =
-//               row) and store the band's partial P rows.
-//
-// Work split: a row band of 128 rows is shared by G CTAs, each owning a
-// contiguous range of 32-column chunks, so the partial count is G (about
-// 148 / bands), not m / 256 -- the P reduce that follows reads G partials.
-// Both operands are K-major with the 128-B swizzle: 8-row core groups 1024 B
-// apart (SBO), the K step of 8 tf32 = 32 B inside the swizzle row.
+//   warp 1      MMA issuer (one thread): per stage and per 8-wide K step,
+//               tcgen05.mma.kind::tf32 A_lo.F_hi + A_hi.F_lo + A_hi.F_hi
+//               (fp32-level accuracy) into a 128 x R fp32 accumulator in TENSOR
+//               MEMORY; tcgen05.commit frees the stage back to the producer.
+//   epilogue    the converter warps drain the accumulator (tcgen05.ld, lane =
+//               output row) into fp32 registers every 256 terms and store the
+//               band's partial rows.
+// Work split: a band of 128 output rows is shared by G CTAs, each owning a
+// contiguous range of 32-wide K chunks (G = the smallest count that keeps the
+// persistent grid busy), so the reduce that follows reads G partials.
 #include "occ_internal.h"
 #include "occ_kernels.cuh"
 #include "occ_v2.cuh"
