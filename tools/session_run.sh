@@ -1,6 +1,8 @@
 set -u
 mkdir -p gpurun_out
-o=gpurun_out/s4e
+o=gpurun_out/s4f
+timeout 300 python tools/umma_acc.py OCC_UMMA=1 > ${o}_acc.jsonl 2>&1; cut -c1-220 ${o}_acc.jsonl
+SHAPE=3072x12288x64 timeout 300 python tools/umma_acc.py OCC_UMMA=1 > ${o}_acc64.jsonl 2>&1; cut -c1-220 ${o}_acc64.jsonl
 timeout 1200 python -m pytest tests -m gpu -q > ${o}_pytest.log 2>&1; echo "pytest rc=$?"; grep -E "FAILED|passed|failed" ${o}_pytest.log | head
-for pdl in 1 0; do OCC_V2_PDL=$pdl timeout 600 python bench.py --steps 200 --warmup 10 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); t=d['north_star_target']; print('pdl=$pdl', d['ms_per_step'], d['eager_ms_per_step'], d['roofline']['frac'], t['ms_per_step'], t['eager_ms_per_step'], t['roofline_frac'])"; done
-for pdl in 1 0; do OCC_V2_PDL=$pdl python tools/graph_probe.py T; done
+for at in 1 0; do for c in C3 C4; do OCC_UMMA_ATMEM=$at timeout 600 python bench.py --config $c --steps 50 --warmup 5 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('at=$at', d['config']['config'], d['ms_per_step'], d['roofline']['frac'])"; done; done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:umma_sweep -c 8 --csv --log-file ${o}_sw.csv python tools/dp_driver.py 2 > /dev/null 2>&1; grep -o '"[0-9]*"$' ${o}_sw.csv | tr '\n' ' '
